@@ -1,0 +1,164 @@
+/*
+ * eis.h -- C ABI of the B200 Eisenstein-discriminant classifier.
+ *
+ * Breuer & Punch, "Quadratic units and cubic fields", arXiv 2507.06579.
+ * Citations are /root/reference/PAPER.md line numbers (the paper's LaTeX).
+ *
+ * The problem (Sec. 1):
+ *   D = { d > 0 : d = 5 (mod 8), d squarefree },
+ *   E = { d in D : eps_d = 1 (mod 2 O_K) },  eps_d the fundamental unit of Q(sqrt d),
+ *   pi_D(x) = #{d in D : d <= x},  pi_E(x) = #{d in E : d <= x}.
+ * The paper computes pi_E(x) for x <= 1e11 with the
+ * residue-tracking infrastructure method of its Appendix (PAPER.md
+ * l.535-756): the generator of each reduced principal ideal is carried only
+ * as its class in (O_K/2O_K)^* = F_4^* = Z/3 (l.601-603), with continued-
+ * fraction baby steps rho (l.541), and NUCOMP/NUDUPL giant steps (l.617-756).
+ *
+ * Residue labelling (one fixed choice, reading R3): an element
+ * a*1 + b*w of O_K, w = (1+sqrt d)/2, with (a mod 2, b mod 2) = (1,0), (0,1),
+ * (1,1) has residue t = 0, 1, 2.  d in E  <=>  t(eps_d) = 0.
+ *
+ * Conventions for every entry point:
+ *  - Return 0 (EIS_OK) on success or a negative EIS_E* code; no exception or
+ *    abort crosses the ABI.  eis_last_error() then describes the failure.
+ *  - Candidates are the integers d = 5 (mod 8); candidate index i <-> d = 8i+5.
+ *  - Host pointers are owned by the caller and only read/written during the
+ *    call (the call is synchronous).  Device pointers (the *_dev variants) are
+ *    owned by the caller, must be device memory on the library's current
+ *    device, and are accessed asynchronously on `stream` (a cudaStream_t
+ *    passed as void*; NULL = the legacy default stream); the caller
+ *    synchronises.
+ *  - The library owns its device scratch (prime table, survivor lists,
+ *    counters) until eis_finalize().
+ *  - Calls are NOT reentrant and not thread-safe: serialise them per process.
+ *  - Every computation runs in the library's CUDA kernels for sm_100a; there
+ *    is no CPU fallback.  Without a usable device every compute call fails
+ *    with EIS_EDEVICE.
+ */
+#ifndef EIS_H
+#define EIS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define EIS_API __attribute__((visibility("default")))
+#else
+#define EIS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Largest d accepted.  The 32-bit baby-step and float-quotient bounds
+ * (sqrt d < 2^19, Q < 2 sqrt d < 2^20) and the int64 giant-step bounds were
+ * validated up to here ("at least for d <= 10^11"). */
+#define EIS_MAX_D 100000000000ULL
+
+/* flag value of a candidate d = 5 (mod 8) that is not squarefree (d not in D) */
+#define EIS_NOT_IN_D 0xFF
+
+enum {
+    EIS_OK = 0,
+    EIS_EINVAL = -1,     /* bad argument: lo > hi, unsorted x, short buffer, NULL */
+    EIS_ERANGE = -2,     /* d > EIS_MAX_D requested */
+    EIS_ENOMEM = -3,     /* device allocation failed */
+    EIS_EDEVICE = -4,    /* no CUDA device / CUDA error / kernel fault */
+    EIS_EINTERNAL = -5   /* an in-kernel invariant failed (a bug; never expected) */
+};
+
+/* Walk modes (eis_set_option("mode", m)).
+ *  EIS_MODE_HALF: baby steps rho from (1) with the symmetry
+ *    exit of Algorithm 1 (l.553-556) and no giant steps: half a period.
+ *  EIS_MODE_BSGS: the paper's Algorithm 1 (l.543-574) with NUCOMPchoose
+ *    giant steps (l.733-756), residues in Z/3 (l.585-603).
+ *  EIS_MODE_AUTO: HALF for d below the crossover (option "crossover"), else BSGS.
+ * All modes return identical results (tests/test_gpu_parity.py). */
+enum { EIS_MODE_AUTO = 0, EIS_MODE_HALF = 1, EIS_MODE_BSGS = 2 };
+
+/* Select the CUDA device this process uses (device < 0: keep the current
+ * one) and build the prime table.  Idempotent; called implicitly by the
+ * compute entry points.  Returns EIS_EDEVICE if no device is usable. */
+EIS_API int eis_init(int device);
+
+/* Release all library-owned device memory and streams. */
+EIS_API void eis_finalize(void);
+
+/* Human-readable description of the last failure in this process; owned by
+ * the library, valid until the next call. */
+EIS_API const char *eis_last_error(void);
+
+/* Tunables (keys: "mode", "crossover", "alpha_x16", "segment_log2",
+ * "blocks_per_sm", "threads"); unknown key or bad value -> EIS_EINVAL. */
+EIS_API int eis_set_option(const char *key, int64_t value);
+EIS_API int64_t eis_get_option(const char *key);
+
+/* Number of candidates d = 5 (mod 8) with lo <= d <= hi (0 if lo > hi). */
+EIS_API size_t eis_num_candidates(uint64_t lo, uint64_t hi);
+
+/* Per-d classification.
+ * out[i] describes d_i = first + 8 i, first = least d >= lo with d = 5 mod 8,
+ * for every d_i <= hi: out[i] = t(eps_{d_i}) in {0,1,2} (d_i in E iff 0),
+ * or EIS_NOT_IN_D if d_i is not squarefree.
+ * out_len must be >= eis_num_candidates(lo, hi) (EIS_EINVAL otherwise);
+ * hi > EIS_MAX_D -> EIS_ERANGE; lo > hi -> EIS_EINVAL.  out may be NULL only
+ * if the range holds no candidate. */
+EIS_API int eis_classify_range(uint64_t lo, uint64_t hi, uint8_t *out, size_t out_len);
+
+/* Counting functions at checkpoints.
+ * x[0..n-1] strictly ascending, 0 < x[0], x[n-1] <= EIS_MAX_D.
+ * pi_D[i] = #{d in D : d <= x[i]},  pi_E[i] = #{d in E : d <= x[i]}.
+ * Equivalent to eis_count_window(0, x, n, pi_D, pi_E).  n == 0 is a no-op. */
+EIS_API int eis_count(const uint64_t *x, size_t n, uint64_t *pi_D, uint64_t *pi_E);
+
+/* Window form (Table 1's windows; the d ~ 1e10 metric):
+ * lo < x[0] < ... < x[n-1] <= EIS_MAX_D,
+ * cnt_D[i] = #{d in D : lo < d <= x[i]},  cnt_E[i] likewise for E. */
+EIS_API int eis_count_window(uint64_t lo, const uint64_t *x, size_t n, uint64_t *cnt_D,
+                     uint64_t *cnt_E);
+
+/* ---- device-resident variants (multi-GPU path: one process per GPU) ---- */
+
+/* Accumulate per-bucket counts of d in (lo, hi] into bucket_dev[0..2n-1]:
+ * bucket_dev[b] += #{d in D, lo < d <= hi, bucket(d) = b} and
+ * bucket_dev[n+b] += the same for E, where bucket(d) = least b with
+ * d <= x[b].  d > x[n-1] are not counted.  x: n uint64 checkpoints in HOST
+ * memory, strictly ascending, x[n-1] <= EIS_MAX_D (the library copies them;
+ * the host needs them to cut segments).  bucket_dev (device memory, 2n
+ * uint64) is NOT zeroed.  Kernels run on `stream`; the call returns after
+ * they finish (it reads back an invariant-violation counter per segment).
+ * Buckets of disjoint (lo, hi] shards sum (e.g. by an NCCL allreduce) to the
+ * buckets of their union. */
+EIS_API int eis_count_buckets_dev(uint64_t lo, uint64_t hi, const uint64_t *x, size_t n,
+                                  uint64_t *bucket_dev, void *stream);
+
+/* Inclusive prefix sums of 2 arrays of n buckets: out_dev[k] =
+ * sum_{b<=k} bucket_dev[b], out_dev[n+k] = sum_{b<=k} bucket_dev[n+b].
+ * Async on `stream`; out_dev may equal bucket_dev. */
+EIS_API int eis_prefix_dev(const uint64_t *bucket_dev, size_t n, uint64_t *out_dev, void *stream);
+
+/* eis_classify_range into device memory out_dev (out_len bytes), async. */
+EIS_API int eis_classify_range_dev(uint64_t lo, uint64_t hi, uint8_t *out_dev, size_t out_len,
+                           void *stream);
+
+/* ---- instrumentation ---- */
+typedef struct {
+    uint64_t d_classified;   /* d in D walked by the last compute call */
+    uint64_t baby_steps;     /* rho steps, all modes */
+    uint64_t giant_steps;    /* NUCOMPchoose calls (BSGS) */
+    uint64_t reduce_steps;   /* rho steps reducing giant-step results */
+    uint64_t sym_exits;      /* d finished by the symmetry exit */
+    uint64_t fallbacks;      /* d re-walked by the half-walk after a BSGS bail-out */
+    uint64_t kernel_launches;/* kernels launched by the last call */
+    double walk_ms;          /* device time of the walk kernels (CUDA events) */
+    double total_ms;         /* device time of the whole call */
+} eis_stats;
+
+/* Counters of the most recent compute call (synchronises the device). */
+EIS_API int eis_get_stats(eis_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EIS_H */

@@ -1,0 +1,68 @@
+// common.cuh -- shared device helpers of the sm_100a Eisenstein classifier.
+// (No code is shared with oracle/: this is the product path only.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef uint32_t u32;
+typedef int32_t i32;
+typedef uint8_t u8;
+
+#define FULL_MASK 0xffffffffu
+
+// Candidate index i <-> d = 8 i + 5 (every d in D is = 5 mod 8).
+__host__ __device__ __forceinline__ u64 cand_d(u64 i) { return 8 * i + 5; }
+
+// floor(sqrt(d)) exactly for d < 2^53 (fp64 sqrt is within 1 ulp; two fixes).
+__device__ __forceinline__ u32 isqrt_u64_dev(u64 d) {
+    u64 s = (u64)sqrt((double)d);
+    while (s * s > d) --s;
+    while ((s + 1) * (s + 1) <= d) ++s;
+    return (u32)s;
+}
+
+// Segment-local checkpoint histogram capacity (buckets per segment).
+constexpr int HIST_CAP = 1024;
+
+// Arguments shared by the walk kernels.
+struct WalkArgs {
+    u64 i0;              // candidate index of segment offset 0
+    const u32 *list;     // survivor offsets (d in D) within the segment
+    const u32 *count;    // device: number of survivors
+    u32 *work;           // device: work counter (zeroed before launch)
+    u8 *flags;           // nullable: flags[off] = t for survivors
+    const u64 *ckpt;     // nullable: checkpoints x[0..n_ckpt)
+    int b_lo, nb;        // bucket range of this segment: [b_lo, b_lo+nb)
+    int n_ckpt;
+    u64 *buckets;        // device: [n_ckpt] D counts then [n_ckpt] E counts
+    u64 *stats;          // device: EisStatSlot counters
+    u32 *err;            // device: invariant-violation counter
+};
+
+enum EisStatSlot {
+    ST_D = 0, ST_BABY = 1, ST_GIANT = 2, ST_REDUCE = 3, ST_SYM = 4, ST_FALLBACK = 5,
+    ST_NSLOTS = 8
+};
+
+// least b in [lo, hi] with d <= x[b]  (caller guarantees d <= x[hi])
+__device__ __forceinline__ int bucket_of(const u64 *x, int lo, int hi, u64 d) {
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (d <= __ldg(x + mid)) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    return v;
+}

@@ -1,0 +1,489 @@
+// eis_api.cu -- C ABI (include/eis.h) of the B200 Eisenstein classifier.
+//
+// Host runtime: validates arguments, owns device scratch, splits the candidate
+// range into segments, and launches per segment
+//   K1+K2 sieve_compact_kernel  (sieve.cuh)       -> survivor list
+//   K3+K4 walk kernel            (walk_*.cuh)     -> flags and/or bucket counts
+// and finally the prefix kernel for the counting functions.  Everything the
+// method computes runs in these kernels; the host only does index arithmetic.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/eis.h"
+#include "common.cuh"
+#include "sieve.cuh"
+#include "walk_half.cuh"
+#include "walk_bsgs.cuh"
+
+namespace {
+
+struct Ctx {
+    bool inited = false;
+    int device = -1;
+    int num_sms = 0;
+    std::vector<u32> h_primes;       // odd primes p <= isqrt(EIS_MAX_D)
+    u32 *d_primes = nullptr;
+    u32 *d_list = nullptr;
+    size_t list_cap = 0;
+    u32 *d_ctr = nullptr;            // [0] survivor count, [1] work counter, [2] err, [3] work2
+    u8 *d_flags = nullptr;
+    size_t flags_cap = 0;
+    u64 *d_x = nullptr;
+    size_t x_cap = 0;
+    u64 *d_buckets = nullptr;
+    size_t buckets_cap = 0;
+    u64 *d_stats = nullptr;
+    BsgsScratch bsgs;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // options
+    int mode = EIS_MODE_AUTO;
+    u64 crossover = ~0ULL;           // AUTO: HALF below, BSGS at/above (set once BSGS lands)
+    int alpha_x16 = 16;              // BSGS baby window W = alpha * d^(1/4)
+    int segment_log2 = 25;
+    int blocks_per_sm = 8;
+    int threads = 256;
+    // instrumentation of the last call
+    eis_stats last{};
+    float walk_ms_acc = 0.f;
+    int launches = 0;
+};
+
+Ctx g;
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(e_ == cudaErrorMemoryAllocation ? EIS_ENOMEM : EIS_EDEVICE,        \
+                        "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                         \
+    } while (0)
+
+u64 isqrt_host(u64 n) {
+    u64 s = (u64)std::sqrt((double)n);
+    while (s * s > n) --s;
+    while ((s + 1) * (s + 1) <= n) ++s;
+    return s;
+}
+
+void build_primes(std::vector<u32> &out) {
+    const u32 M = (u32)isqrt_host(EIS_MAX_D);
+    std::vector<uint8_t> comp(M + 1, 0);
+    out.clear();
+    for (u32 i = 2; i <= M; i++) {
+        if (comp[i]) continue;
+        if (i != 2) out.push_back(i);
+        for (u64 j = (u64)i * i; j <= M; j += i) comp[j] = 1;
+    }
+}
+
+template <class T>
+int ensure(T *&ptr, size_t &cap, size_t n) {
+    if (n <= cap && ptr) return 0;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    size_t want = std::max(n, (size_t)1);
+    CUDA_TRY(cudaMalloc(&ptr, want * sizeof(T)));
+    cap = want;
+    return 0;
+}
+
+int do_init(int device) {
+    if (g.inited && (device < 0 || device == g.device)) return 0;
+    if (g.inited) eis_finalize();
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(EIS_EDEVICE, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device >= 0) CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaGetDevice(&g.device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, g.device));
+    if (prop.major < 10)
+        return fail(EIS_EDEVICE, "device %d is sm_%d%d; this library is built for sm_100a",
+                    g.device, prop.major, prop.minor);
+    g.num_sms = prop.multiProcessorCount;
+    build_primes(g.h_primes);
+    CUDA_TRY(cudaMalloc(&g.d_primes, g.h_primes.size() * sizeof(u32)));
+    CUDA_TRY(cudaMemcpy(g.d_primes, g.h_primes.data(), g.h_primes.size() * sizeof(u32),
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&g.d_ctr, 16 * sizeof(u32)));
+    CUDA_TRY(cudaMalloc(&g.d_stats, ST_NSLOTS * sizeof(u64)));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    for (auto &ev : g.ev) CUDA_TRY(cudaEventCreate(&ev));
+    CUDA_TRY(cudaFuncSetAttribute(sieve_compact_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SIEVE_WORDS * (int)sizeof(u32)));
+    g.inited = true;
+    return 0;
+}
+
+// number of odd primes p with p^2 <= v
+int primes_upto_sq(u64 v) {
+    u64 r = isqrt_host(v);
+    return (int)(std::upper_bound(g.h_primes.begin(), g.h_primes.end(), (u32)std::min<u64>(r, 0xFFFFFFFFull)) -
+                 g.h_primes.begin());
+}
+int primes_small() {   // p^2 <= SIEVE_CHUNK
+    return primes_upto_sq((u64)SIEVE_CHUNK);
+}
+
+// candidate index range [i_first, i_last] for lo <= d <= hi; false if empty
+bool cand_range(u64 lo, u64 hi, u64 &i_first, u64 &i_last) {
+    if (lo > hi || hi < 5) return false;
+    const u64 L = lo < 5 ? 5 : lo;
+    const u64 first = L + (13 - L % 8) % 8;   // least d >= L with d = 5 mod 8
+    if (first > hi) return false;
+    i_first = (first - 5) / 8;
+    i_last = (hi - 5) / 8;
+    return true;
+}
+
+bool want_bsgs(u64 d_lo) {
+    if (g.mode == EIS_MODE_HALF) return false;
+    if (g.mode == EIS_MODE_BSGS) return true;
+    return d_lo >= g.crossover;
+}
+
+// Process candidates [i_first, i_last].  flags_dev (nullable) is indexed by
+// candidate index - i_first.  x_host/x_dev/n/buckets_dev (nullable) receive counts.
+int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u64 *x_dev,
+              int n, u64 *buckets_dev, cudaStream_t s) {
+    const u64 SEG = 1ull << g.segment_log2;
+    const int n_small = primes_small();
+    for (u64 seg = i_first; seg <= i_last;) {
+        u64 len = std::min(SEG, i_last - seg + 1);
+        int b_lo = 0, nb = 0;
+        if (x_host) {
+            // bucket span of [d(seg), d(seg+len-1)] must fit HIST_CAP
+            u64 d0 = cand_d(seg);
+            b_lo = (int)(std::lower_bound(x_host, x_host + n, d0) - x_host);
+            if (b_lo >= n) break;   // beyond the last checkpoint
+            u64 dlast = cand_d(seg + len - 1);
+            int b_hi = (int)(std::lower_bound(x_host, x_host + n, dlast) - x_host);
+            if (b_hi >= n) {   // clip to the last checkpoint
+                b_hi = n - 1;
+                if (x_host[n - 1] < d0) break;
+                len = (x_host[n - 1] - 5) / 8 - seg + 1;
+            }
+            if (b_hi - b_lo + 1 > HIST_CAP) {
+                b_hi = b_lo + HIST_CAP - 1;
+                u64 lim = x_host[b_hi];            // last d allowed: <= x[b_hi]
+                len = (lim - 5) / 8 - seg + 1;
+            }
+            nb = b_hi - b_lo + 1;
+        }
+        const u64 d_last = cand_d(seg + len - 1);
+        const int n_primes = primes_upto_sq(d_last);
+        if (ensure(g.d_list, g.list_cap, (size_t)len)) return EIS_ENOMEM;
+        CUDA_TRY(cudaMemsetAsync(g.d_ctr, 0, 16 * sizeof(u32), s));
+        const unsigned sblocks = (unsigned)((len + SIEVE_CHUNK - 1) / SIEVE_CHUNK);
+        u8 *fseg = flags_dev ? flags_dev + (seg - i_first) : nullptr;
+        sieve_compact_kernel<<<sblocks, SIEVE_THREADS, SIEVE_WORDS * sizeof(u32), s>>>(
+            seg, len, g.d_primes, std::min(n_small, n_primes), n_primes, g.d_list, g.d_ctr,
+            fseg);
+        CUDA_TRY(cudaGetLastError());
+        g.launches++;
+
+        WalkArgs a;
+        a.i0 = seg;
+        a.list = g.d_list;
+        a.count = g.d_ctr;
+        a.work = g.d_ctr + 1;
+        a.err = g.d_ctr + 2;
+        a.flags = fseg;
+        a.ckpt = x_host ? x_dev : nullptr;
+        a.b_lo = b_lo;
+        a.nb = nb;
+        a.n_ckpt = n;
+        a.buckets = buckets_dev;
+        a.stats = g.d_stats;
+        CUDA_TRY(cudaEventRecord(g.ev[2], s));
+        if (want_bsgs(cand_d(seg))) {
+            int rc = launch_bsgs(a, cand_d(seg), d_last, g.num_sms, g.alpha_x16, g.bsgs,
+                                 g.d_ctr + 3, s, &g.launches);
+            if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
+                              : fail(EIS_EDEVICE, "BSGS launch failed: %s",
+                                     cudaGetErrorString(cudaGetLastError()));
+        } else {
+            const unsigned wblocks = (unsigned)(g.num_sms * g.blocks_per_sm);
+            walk_half_kernel<32><<<wblocks, 256, 0, s>>>(a);
+            CUDA_TRY(cudaGetLastError());
+            g.launches++;
+        }
+        CUDA_TRY(cudaEventRecord(g.ev[3], s));
+        CUDA_TRY(cudaEventSynchronize(g.ev[3]));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, g.ev[2], g.ev[3]);
+        g.walk_ms_acc += ms;
+        u32 err = 0;
+        CUDA_TRY(cudaMemcpy(&err, g.d_ctr + 2, sizeof(u32), cudaMemcpyDeviceToHost));
+        if (err) return fail(EIS_EINTERNAL, "%u in-kernel invariant violations in segment at d=%llu",
+                             err, (unsigned long long)cand_d(seg));
+        seg += len;
+    }
+    return 0;
+}
+
+__global__ void prefix_kernel(const u64 *in, u64 *out, int n) {
+    // one CTA of 1024 threads: two independent inclusive scans of length n
+    __shared__ u64 part[1024];
+    for (int arr = 0; arr < 2; arr++) {
+        const u64 *src = in + (size_t)arr * n;
+        u64 *dst = out + (size_t)arr * n;
+        const int per = (n + 1023) / 1024;
+        const int b = threadIdx.x * per, e = min(n, b + per);
+        u64 acc = 0;
+        for (int i = b; i < e; i++) acc += src[i];
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            u64 v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+            __syncthreads();
+            part[threadIdx.x] += v;
+            __syncthreads();
+        }
+        u64 run = part[threadIdx.x] - acc;
+        __syncthreads();
+        for (int i = b; i < e; i++) { run += src[i]; dst[i] = run; }
+        __syncthreads();
+    }
+}
+
+int begin_call(cudaStream_t s) {
+    g.walk_ms_acc = 0;
+    g.launches = 0;
+    CUDA_TRY(cudaMemsetAsync(g.d_stats, 0, ST_NSLOTS * sizeof(u64), s));
+    CUDA_TRY(cudaEventRecord(g.ev[0], s));
+    return 0;
+}
+
+int end_call(cudaStream_t s) {
+    CUDA_TRY(cudaEventRecord(g.ev[1], s));
+    CUDA_TRY(cudaEventSynchronize(g.ev[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g.ev[0], g.ev[1]);
+    u64 st[ST_NSLOTS];
+    CUDA_TRY(cudaMemcpy(st, g.d_stats, sizeof st, cudaMemcpyDeviceToHost));
+    g.last.d_classified = st[ST_D];
+    g.last.baby_steps = st[ST_BABY];
+    g.last.giant_steps = st[ST_GIANT];
+    g.last.reduce_steps = st[ST_REDUCE];
+    g.last.sym_exits = st[ST_SYM];
+    g.last.fallbacks = st[ST_FALLBACK];
+    g.last.kernel_launches = (u64)g.launches;
+    g.last.walk_ms = g.walk_ms_acc;
+    g.last.total_ms = ms;
+    return 0;
+}
+
+int check_x(const u64 *x, size_t n, u64 lo) {
+    if (n == 0) return 0;
+    if (!x) return fail(EIS_EINVAL, "x is NULL");
+    if (x[0] <= lo) return fail(EIS_EINVAL, "x[0]=%llu must exceed lo=%llu",
+                                (unsigned long long)x[0], (unsigned long long)lo);
+    for (size_t i = 1; i < n; i++)
+        if (x[i] <= x[i - 1]) return fail(EIS_EINVAL, "x must be strictly ascending (x[%zu])", i);
+    if (x[n - 1] > EIS_MAX_D)
+        return fail(EIS_ERANGE, "x[n-1]=%llu exceeds EIS_MAX_D", (unsigned long long)x[n - 1]);
+    if (n > (size_t)1 << 30) return fail(EIS_EINVAL, "too many checkpoints");
+    return 0;
+}
+
+int count_buckets(u64 lo, u64 hi, const u64 *x, size_t n, u64 *buckets_dev, cudaStream_t s) {
+    if (n == 0 || hi <= lo) return 0;
+    if (ensure(g.d_x, g.x_cap, n)) return EIS_ENOMEM;
+    CUDA_TRY(cudaMemcpyAsync(g.d_x, x, n * sizeof(u64), cudaMemcpyHostToDevice, s));
+    u64 top = std::min(hi, x[n - 1]);
+    u64 i_first, i_last;
+    if (!cand_range(lo + 1, top, i_first, i_last)) return 0;
+    return run_range(i_first, i_last, nullptr, x, g.d_x, (int)n, buckets_dev, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int eis_init(int device) { return do_init(device); }
+
+void eis_finalize(void) {
+    if (!g.inited) return;
+    cudaFree(g.d_primes);
+    cudaFree(g.d_list);
+    cudaFree(g.d_ctr);
+    cudaFree(g.d_flags);
+    cudaFree(g.d_x);
+    cudaFree(g.d_buckets);
+    cudaFree(g.d_stats);
+    bsgs_free(g.bsgs);
+    for (auto &ev : g.ev) if (ev) cudaEventDestroy(ev);
+    if (g.stream) cudaStreamDestroy(g.stream);
+    Ctx fresh;
+    fresh.mode = g.mode;
+    fresh.crossover = g.crossover;
+    fresh.alpha_x16 = g.alpha_x16;
+    fresh.segment_log2 = g.segment_log2;
+    fresh.blocks_per_sm = g.blocks_per_sm;
+    g = fresh;
+}
+
+const char *eis_last_error(void) { return g_err.c_str(); }
+
+int eis_set_option(const char *key, int64_t v) {
+    if (!key) return fail(EIS_EINVAL, "NULL key");
+    std::string k(key);
+    if (k == "mode") {
+        if (v < 0 || v > 2) return fail(EIS_EINVAL, "mode must be 0..2");
+        g.mode = (int)v;
+    } else if (k == "crossover") {
+        if (v < 0) return fail(EIS_EINVAL, "crossover must be >= 0");
+        g.crossover = (u64)v;
+    } else if (k == "alpha_x16") {
+        if (v < 4 || v > 256) return fail(EIS_EINVAL, "alpha_x16 must be in [4, 256]");
+        g.alpha_x16 = (int)v;
+    } else if (k == "segment_log2") {
+        if (v < 18 || v > 31) return fail(EIS_EINVAL, "segment_log2 must be in [18, 31]");
+        g.segment_log2 = (int)v;
+    } else if (k == "blocks_per_sm") {
+        if (v < 1 || v > 32) return fail(EIS_EINVAL, "blocks_per_sm must be in [1, 32]");
+        g.blocks_per_sm = (int)v;
+    } else {
+        return fail(EIS_EINVAL, "unknown option '%s'", key);
+    }
+    return 0;
+}
+
+int64_t eis_get_option(const char *key) {
+    if (!key) return fail(EIS_EINVAL, "NULL key");
+    std::string k(key);
+    if (k == "mode") return g.mode;
+    if (k == "crossover") return (int64_t)g.crossover;
+    if (k == "alpha_x16") return g.alpha_x16;
+    if (k == "segment_log2") return g.segment_log2;
+    if (k == "blocks_per_sm") return g.blocks_per_sm;
+    return fail(EIS_EINVAL, "unknown option '%s'", key);
+}
+
+size_t eis_num_candidates(uint64_t lo, uint64_t hi) {
+    u64 a, b;
+    if (!cand_range(lo, hi, a, b)) return 0;
+    return (size_t)(b - a + 1);
+}
+
+int eis_classify_range_dev(uint64_t lo, uint64_t hi, uint8_t *out_dev, size_t out_len,
+                           void *stream) {
+    if (lo > hi) return fail(EIS_EINVAL, "lo > hi");
+    if (hi > EIS_MAX_D) return fail(EIS_ERANGE, "hi exceeds EIS_MAX_D");
+    size_t n = eis_num_candidates(lo, hi);
+    if (n == 0) return 0;
+    if (!out_dev) return fail(EIS_EINVAL, "out is NULL");
+    if (out_len < n) return fail(EIS_EINVAL, "out_len %zu < %zu candidates", out_len, n);
+    if (int rc = do_init(-1)) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : 0;
+    if (int rc = begin_call(s)) return rc;
+    u64 a, b;
+    cand_range(lo, hi, a, b);
+    if (int rc = run_range(a, b, out_dev, nullptr, nullptr, 0, nullptr, s)) return rc;
+    return end_call(s);
+}
+
+int eis_classify_range(uint64_t lo, uint64_t hi, uint8_t *out, size_t out_len) {
+    if (lo > hi) return fail(EIS_EINVAL, "lo > hi");
+    if (hi > EIS_MAX_D) return fail(EIS_ERANGE, "hi exceeds EIS_MAX_D");
+    size_t n = eis_num_candidates(lo, hi);
+    if (n == 0) return 0;
+    if (!out) return fail(EIS_EINVAL, "out is NULL");
+    if (out_len < n) return fail(EIS_EINVAL, "out_len %zu < %zu candidates", out_len, n);
+    if (int rc = do_init(-1)) return rc;
+    cudaStream_t s = g.stream;
+    if (int rc = begin_call(s)) return rc;
+    u64 a, b;
+    cand_range(lo, hi, a, b);
+    const u64 SEG = 1ull << g.segment_log2;
+    if (ensure(g.d_flags, g.flags_cap, (size_t)std::min<u64>(SEG, n))) return EIS_ENOMEM;
+    for (u64 seg = a; seg <= b; seg += SEG) {
+        u64 e = std::min(b, seg + SEG - 1);
+        if (int rc = run_range(seg, e, g.d_flags, nullptr, nullptr, 0, nullptr, s)) return rc;
+        CUDA_TRY(cudaMemcpyAsync(out + (seg - a), g.d_flags, (size_t)(e - seg + 1),
+                                 cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return end_call(s);
+}
+
+int eis_count_buckets_dev(uint64_t lo, uint64_t hi, const uint64_t *x, size_t n,
+                          uint64_t *bucket_dev, void *stream) {
+    if (int rc = check_x(x, n, 0)) return rc;
+    if (n && !bucket_dev) return fail(EIS_EINVAL, "bucket_dev is NULL");
+    if (hi > EIS_MAX_D) return fail(EIS_ERANGE, "hi exceeds EIS_MAX_D");
+    if (lo > hi) return fail(EIS_EINVAL, "lo > hi");
+    if (int rc = do_init(-1)) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : 0;
+    if (int rc = begin_call(s)) return rc;
+    if (int rc = count_buckets(lo, hi, x, n, bucket_dev, s)) return rc;
+    return end_call(s);
+}
+
+int eis_prefix_dev(const uint64_t *bucket_dev, size_t n, uint64_t *out_dev, void *stream) {
+    if (n == 0) return 0;
+    if (!bucket_dev || !out_dev) return fail(EIS_EINVAL, "NULL pointer");
+    if (int rc = do_init(-1)) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : 0;
+    prefix_kernel<<<1, 1024, 0, s>>>(bucket_dev, out_dev, (int)n);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int eis_count_window(uint64_t lo, const uint64_t *x, size_t n, uint64_t *cnt_D,
+                     uint64_t *cnt_E) {
+    if (n == 0) return 0;
+    if (int rc = check_x(x, n, lo)) return rc;
+    if (!cnt_D || !cnt_E) return fail(EIS_EINVAL, "NULL output");
+    if (int rc = do_init(-1)) return rc;
+    cudaStream_t s = g.stream;
+    if (int rc = begin_call(s)) return rc;
+    if (ensure(g.d_buckets, g.buckets_cap, 2 * n)) return EIS_ENOMEM;
+    CUDA_TRY(cudaMemsetAsync(g.d_buckets, 0, 2 * n * sizeof(u64), s));
+    if (int rc = count_buckets(lo, x[n - 1], x, n, g.d_buckets, s)) return rc;
+    prefix_kernel<<<1, 1024, 0, s>>>(g.d_buckets, g.d_buckets, (int)n);
+    CUDA_TRY(cudaGetLastError());
+    g.launches++;
+    std::vector<u64> h(2 * n);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), g.d_buckets, 2 * n * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    if (int rc = end_call(s)) return rc;
+    std::memcpy(cnt_D, h.data(), n * sizeof(u64));
+    std::memcpy(cnt_E, h.data() + n, n * sizeof(u64));
+    return 0;
+}
+
+int eis_count(const uint64_t *x, size_t n, uint64_t *pi_D, uint64_t *pi_E) {
+    return eis_count_window(0, x, n, pi_D, pi_E);
+}
+
+int eis_get_stats(eis_stats *out) {
+    if (!out) return fail(EIS_EINVAL, "NULL out");
+    *out = g.last;
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+// walk_half.cuh -- K3 in HALF mode: baby steps rho with the symmetry exit, no giant steps.
+//
+// For each d in D (one lane per d, persistent CTAs, warp-aggregated refill from
+// a global work counter) walk the cycle of reduced principal ideals
+//   (theta_{j+1}) = [Q_j/2, (P_j + sqrt d)/2],  (Q_0, P_0) = (2, 1),  theta_1 = 1,
+// with rho:
+//   q_j = floor((P_j + sqrt d)/Q_j), P_{j+1} = q_j Q_j - P_j, Q_{j+1} = (d - P_{j+1}^2)/Q_j,
+//   theta_{j+2} = ((P_{j+1} + sqrt d)/Q_j) theta_{j+1},
+// carrying theta only as its residue t in Z/3.  Since
+// Q_j = 2 mod 4 and P_{j+1} is odd, (P_{j+1} + sqrt d)/Q_j = ((P-1)/2 + w)/(Q_j/2)
+// has residue 1 if P_{j+1} = 1 mod 4 and 2 if P_{j+1} = 3 mod 4 (R5).
+// The walk stops at the symmetry point of Algorithm 1 (PAPER.md l.553-556,
+// "if Q_j = Q_{j-1} or P_j = P_{j-1}"), where (R7)
+//   Q_j = Q_{j-1}:          t(eps) = t(theta_j) + t(theta_{j+1}),
+//   P_j = P_{j-1}, j >= 2:  t(eps) = 2 t(theta_j).
+//
+// Arithmetic: all u32 (sqrt d < 2^19, Q < 2 sqrt d < 2^20 for d <= 1e11).
+//  * Q_{j+1} = Q_{j-1} + q_j (P_j - P_{j+1}) in wrapping u32 (exact: the true
+//    value is < 2^20), seeded with Q_{-1} = (d - 1)/2 mod 2^32.
+//  * q = floor(num/Q) with num = P + s < 2^20: exact float images by the 2^23
+//    magic-number trick (LOP3 + FADD instead of the narrow I2F pipe), one
+//    MUFU.RCP, one FFMA that rounds num*rcp(Q) to an integer; the result is
+//    floor or floor+1 (|error| < 0.27, K3), fixed by one compare.
+//  * P_{j+1} = q Q - P = s - r with r = num - q Q.
+#pragma once
+#include "common.cuh"
+
+struct BabyState {
+    u32 s, P, Q, Qp;   // isqrt(d), P_j, Q_j, Q_{j-1}
+    u32 m, b;          // steps done, sum of bit1(P) over them: t(theta_{m+1}) = m + b
+};
+
+__device__ __forceinline__ void baby_init(BabyState &st, u64 d) {
+    st.s = isqrt_u64_dev(d);
+    st.P = 1;
+    st.Q = 2;
+    st.Qp = (u32)((d - 1) >> 1);   // Q_{-1} = (d - P_0^2)/Q_0, mod 2^32
+    st.m = 0;
+    st.b = 0;
+}
+
+__device__ __forceinline__ float u32_to_f_exact(u32 v) {   // v < 2^23
+    return __int_as_float((int)(v | 0x4B000000u)) - 8388608.0f;
+}
+
+// One rho step.  Returns true at the symmetry point with *res = t(eps) (not reduced mod 3).
+__device__ __forceinline__ bool baby_step(BabyState &st, u32 *res) {
+    const u32 num = st.P + st.s;
+    const float nf = u32_to_f_exact(num);
+    const float qf = u32_to_f_exact(st.Q);
+    float rq;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"(qf));
+    u32 q = __float_as_uint(fmaf(nf, rq, 8388608.0f)) - 0x4B000000u;   // round(num/Q)
+    i32 r = (i32)(num - q * st.Q);
+    if (r < 0) { q -= 1; r += (i32)st.Q; }
+    const u32 Pn = st.s - (u32)r;
+    const u32 Qn = st.Qp + q * (st.P - Pn);
+    const u32 bit = (Pn >> 1) & 1u;
+    const u32 tc = st.m + st.b;               // t(theta_j)
+    const bool exQ = (Qn == st.Q);
+    const bool exP = (Pn == st.P) && (st.m >= 1);
+    st.m += 1;
+    st.b += bit;
+    st.Qp = st.Q;
+    st.Q = Qn;
+    st.P = Pn;
+    if (exQ | exP) {
+        *res = exQ ? (2 * tc + 1 + bit) : 2 * tc;
+        return true;
+    }
+    return false;
+}
+
+template <int KSTEPS>
+__global__ void __launch_bounds__(256)
+walk_half_kernel(WalkArgs a) {
+    __shared__ u32 hist[2 * HIST_CAP];
+    for (int i = threadIdx.x; i < 2 * a.nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const u32 n = *a.count;
+    BabyState st;
+    u64 d = 0;
+    u32 off = 0;
+    bool active = false, exhausted = false;
+    u32 n_done = 0, n_sym = 0;
+    u64 steps = 0;
+
+    for (;;) {
+        const u32 need = __ballot_sync(FULL_MASK, !active && !exhausted);
+        if (need) {
+            const int leader = __ffs(need) - 1;
+            u32 base = 0;
+            if (lane == leader) base = atomicAdd(a.work, (u32)__popc(need));
+            base = __shfl_sync(FULL_MASK, base, leader);
+            if (!active && !exhausted) {
+                const u32 idx = base + __popc(need & lanemask_lt());
+                if (idx < n) {
+                    off = __ldg(a.list + idx);
+                    d = cand_d(a.i0 + off);
+                    baby_init(st, d);
+                    active = true;
+                } else {
+                    exhausted = true;
+                }
+            }
+        }
+        if (__all_sync(FULL_MASK, exhausted)) break;
+        if (active) {
+            u32 res = 0;
+            bool fin = false;
+#pragma unroll 4
+            for (int k = 0; k < KSTEPS; k++) {
+                if (baby_step(st, &res)) { fin = true; break; }
+            }
+            if (fin) {
+                const u32 t = res % 3;
+                steps += st.m;
+                n_done++;
+                n_sym++;
+                if (a.flags) a.flags[off] = (u8)t;
+                if (a.ckpt) {
+                    const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
+                    atomicAdd(&hist[b], 1u);
+                    if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
+                }
+                active = false;
+            }
+        }
+    }
+
+    // statistics: one atomic per warp
+    u64 s_steps = warp_sum_u64(steps);
+    u64 s_done = warp_sum_u64(n_done);
+    u64 s_sym = warp_sum_u64(n_sym);
+    if (lane == 0 && a.stats) {
+        atomicAdd((unsigned long long *)&a.stats[ST_BABY], (unsigned long long)s_steps);
+        atomicAdd((unsigned long long *)&a.stats[ST_D], (unsigned long long)s_done);
+        atomicAdd((unsigned long long *)&a.stats[ST_SYM], (unsigned long long)s_sym);
+    }
+    __syncthreads();
+    if (a.ckpt) {
+        for (int i = threadIdx.x; i < a.nb; i += blockDim.x) {
+            if (hist[i])
+                atomicAdd((unsigned long long *)&a.buckets[a.b_lo + i], (unsigned long long)hist[i]);
+            if (hist[a.nb + i])
+                atomicAdd((unsigned long long *)&a.buckets[a.n_ckpt + a.b_lo + i],
+                          (unsigned long long)hist[a.nb + i]);
+        }
+    }
+}

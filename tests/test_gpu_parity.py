@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+paper's printed values.  Bit-exact on every per-d flag and every count.
+
+Sizes: the element-by-element comparisons use ranges the oracle finishes in
+seconds that still span many sieve chunks (2^18 candidates), several
+segments (forced small with segment_log2) and ragged ends; the full-size
+configurations (BASELINE.json configs C2-C4, the bench's metric slab) are
+checked on seeded oracle samples, on Table 1 totals and
+on the Moebius closed form of pi_D, at the launch configuration bench.py uses.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2507_06579_b200 as eis
+import workloads
+from oracle import c_oracle
+from pins import paper_windows, pi_D_closed_form
+
+pytestmark = pytest.mark.gpu
+
+MODES = {"half": eis.MODE_HALF, "auto": eis.MODE_AUTO}
+NTHREADS = 0   # oracle: all host cores
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2507_06579_b200 import _build
+
+    _build.build()
+    eis.init(0)
+    yield
+    eis.set_option("mode", eis.MODE_AUTO)
+
+
+@pytest.fixture(params=list(MODES))
+def mode(request):
+    eis.set_option("mode", MODES[request.param])
+    yield request.param
+    eis.set_option("mode", eis.MODE_AUTO)
+
+
+def _flags_equal(lo, hi, got=None):
+    got = eis.classify_range(lo, hi) if got is None else got
+    want = c_oracle.classify_range(lo, hi, NTHREADS)
+    assert got.shape == want.shape
+    bad = np.flatnonzero(got != want)
+    first = lo + (5 - lo) % 8
+    assert bad.size == 0, [(first + 8 * int(i), int(got[i]), int(want[i])) for i in bad[:10]]
+    return got
+
+
+def test_flags_prefix_1e6(mode):
+    f = _flags_equal(0, 10**6)
+    assert int((f == 0).sum()) == c_oracle.count_window(0, [10**6])[1][0]
+
+
+@pytest.mark.parametrize("lo,hi", [
+    (10**7 - 123_457, 10**7 + 77_777),            # ragged ends around 1e7
+    (10**8 - 65_001, 10**8 + 3),                  # ~8k candidates at 1e8
+    (10**9 - 16_003, 10**9 + 9),                  # 1e9
+    (10**10 - 6_001, 10**10),                     # 1e10
+    (eis.MAX_D - 1_203, eis.MAX_D),               # the top: 10^11
+])
+def test_flags_windows(mode, lo, hi):
+    _flags_equal(lo, hi)
+
+
+def test_edge_cases(mode):
+    assert list(eis.classify_range(5, 5)) == [1]              # eps_5 = (1+sqrt5)/2, t=1
+    assert list(eis.classify_range(45, 45)) == [eis.NOT_IN_D]  # 9 | 45
+    assert list(eis.classify_range(661, 661)) == [2]          # t=2
+    assert list(eis.classify_range(1901, 1901)) == [0]        # in E
+    assert list(eis.classify_range(7053, 7053)) == [0]        # in E
+    assert eis.classify_range(6, 12).size == 0
+    assert eis.classify_range(0, 4).size == 0
+    cD, cE = eis.count([4])
+    assert list(cD) == [0] and list(cE) == [0]
+    cD, cE = eis.count([5, 37])
+    assert list(cD) == [1, 5] and list(cE) == [0, 1]          # 37: least d in E
+    # window whose only candidates are non-squarefree: 45 (9*5), 117 (9*13)
+    cD, cE = eis.count_window(44, [45])
+    assert list(cD) == [0]
+
+
+def test_segments_and_chunks_are_invisible(mode):
+    """Results do not depend on the segment size (many segments, ragged tails)."""
+    lo, hi = 3_000_001, 7_123_457
+    ref = eis.classify_range(lo, hi)
+    old = eis.get_option("segment_log2")
+    try:
+        eis.set_option("segment_log2", 18)
+        assert np.array_equal(eis.classify_range(lo, hi), ref)
+        x = [4_000_000, 5_000_003, 7_123_457]
+        a = eis.count_window(lo, x)
+        eis.set_option("segment_log2", old)
+        b = eis.count_window(lo, x)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    finally:
+        eis.set_option("segment_log2", old)
+    _flags_equal(lo, hi, ref)
+
+
+def test_count_matches_oracle_and_flags(mode):
+    x = [10, 1000, 12_345, 100_000, 333_333, 10**6]
+    cD, cE = eis.count(x)
+    oD, oE = c_oracle.count_window(0, x, NTHREADS)
+    assert np.array_equal(cD, oD) and np.array_equal(cE, oE)
+    assert [int(v) for v in cD] == [pi_D_closed_form(v) for v in x]
+    # window form
+    wD, wE = eis.count_window(12_345, x[3:])
+    assert np.array_equal(wD, cD[3:] - cD[2]) and np.array_equal(wE, cE[3:] - cE[2])
+    # many checkpoints: more buckets than one segment's histogram holds
+    xs = list(range(100, 400_001, 100))
+    cD, cE = eis.count(xs)
+    oD, oE = c_oracle.count_window(0, xs, NTHREADS)
+    assert np.array_equal(cD, oD) and np.array_equal(cE, oE)
+
+
+def test_determinism(mode):
+    a = eis.classify_range(10**8, 10**8 + 2_000_000)
+    b = eis.classify_range(10**8, 10**8 + 2_000_000)
+    assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------- full-size configurations --
+def test_table1_windows_and_pi_D():
+    """All four Table 1 totals and pi_D by the closed form,
+    in the default (bench) mode."""
+    eis.set_option("mode", eis.MODE_AUTO)
+    for lo, hi, want_E in paper_windows():
+        cD, cE = eis.count_window(lo, [hi])
+        assert int(cE[0]) == want_E, (lo, hi, int(cE[0]), want_E)
+        assert int(cD[0]) == pi_D_closed_form(hi) - pi_D_closed_form(lo), (lo, hi)
+
+
+def test_C2_all_flags_vs_oracle():
+    """BASELINE config C2: every d <= 1e8, per-d flags against the oracle.
+    The oracle costs ~1300 core-seconds here; with few host cores a seeded
+    stratified sample (every k-th candidate from a seeded offset) is used."""
+    eis.set_option("mode", eis.MODE_AUTO)
+    f = eis.classify_range(0, 10**8)
+    assert int((f == 0).sum()) == paper_windows()[0][2]
+    ncpu = os.cpu_count() or 1
+    stride = 1 if ncpu >= 48 or os.environ.get("EIS_FULL_C2") == "1" else 97
+    off = int(np.random.default_rng(workloads.SEED).integers(0, stride))
+    idx = np.arange(off, f.size, stride)
+    want = c_oracle.classify_list(5 + 8 * idx.astype(np.uint64), NTHREADS)
+    bad = np.flatnonzero(f[idx] != want)
+    assert bad.size == 0, [(5 + 8 * int(idx[i]), int(f[idx[i]]), int(want[i])) for i in bad[:10]]
+
+
+def test_C3_checkpoints_and_samples():
+    """BASELINE config C3: d <= 1e9, checkpoints every 1e7: pi_D at all 100
+    checkpoints by the closed form, the Table 1 window (9e8, 1e9], per-d
+    flags of 4000 seeded samples against the oracle, counts == flag sums."""
+    eis.set_option("mode", eis.MODE_AUTO)
+    cfg = workloads.CONFIGS["C3"]
+    cD, cE = eis.count(cfg["x"])
+    for x, v in zip(cfg["x"][9::10], cD[9::10]):
+        assert int(v) == pi_D_closed_form(x), x
+    assert int(cE[-1] - cE[89]) == 3_310_835
+    s = workloads.sample_candidates(0, 10**9, 4000)
+    f = eis.classify_range(0, 10**9)
+    got = f[((s - 5) // 8).astype(np.int64)]
+    want = c_oracle.classify_list(s, NTHREADS)
+    assert np.array_equal(got, want)
+    assert int((f != eis.NOT_IN_D).sum()) == int(cD[-1]) and int((f == 0).sum()) == int(cE[-1])
+
+
+def test_C4_window_top():
+    """BASELINE config C4: window (1e11 - 1e9, 1e11] (longest periods):
+    Table 1 sub-window, pi_D closed form, 150 seeded oracle samples."""
+    eis.set_option("mode", eis.MODE_AUTO)
+    cfg = workloads.CONFIGS["C4"]
+    cD, cE = eis.count_window(cfg["lo"], cfg["x"])
+    assert int(cE[-1] - cE[-2]) == 3_345_503
+    assert int(cD[-1]) == pi_D_closed_form(cfg["hi"]) - pi_D_closed_form(cfg["lo"])
+    s = workloads.sample_candidates(cfg["lo"] + 1, cfg["hi"], 150)
+    got = np.array([eis.classify_range(int(d), int(d))[0] for d in s], dtype=np.uint8)
+    want = c_oracle.classify_list(s, NTHREADS)
+    assert np.array_equal(got, want)
+
+
+def test_metric_slab_as_benched():
+    """The bench workload (slab 0 of the metric window, checkpoints every 1e7)
+    in the bench's launch configuration: Table 1's (9.9e9, 1e10] total and
+    seeded per-d samples."""
+    eis.set_option("mode", eis.MODE_AUTO)
+    lo, hi = workloads.metric_slab(0)
+    x = workloads.metric_checkpoints(1)
+    cD, cE = eis.count_window(lo, x)
+    i99 = x.index(9_900_000_000)
+    assert int(cE[-1] - cE[i99]) == 3_334_227
+    assert int(cD[-1]) == pi_D_closed_form(hi) - pi_D_closed_form(lo)
+    s = workloads.sample_candidates(lo + 1, hi, 600)
+    f = eis.classify_range(lo + 1, hi)
+    got = f[((s - (lo + 1 + (5 - (lo + 1)) % 8)) // 8).astype(np.int64)]
+    want = c_oracle.classify_list(s, NTHREADS)
+    assert np.array_equal(got, want)

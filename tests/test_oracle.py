@@ -23,16 +23,7 @@ import pytest
 from oracle import c_oracle as C
 from oracle import oracle as O
 
-GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
-
-
-def _golden(name):
-    rows = []
-    for line in open(os.path.join(GOLDEN, name)):
-        line = line.split("#")[0].strip()
-        if line:
-            rows.append(line.split())
-    return rows
+from pins import golden as _golden, pi_D_closed_form
 
 
 def D_upto(n):
@@ -152,30 +143,6 @@ def test_non_squarefree_and_invalid_rejected():
 
 
 # ---------------------------------------------------------- pi_D closed form --
-def _mobius_upto(n):
-    mu = np.ones(n + 1, dtype=np.int64)
-    is_p = np.ones(n + 1, dtype=bool)
-    is_p[:2] = False
-    for p in range(2, n + 1):
-        if is_p[p]:
-            is_p[2 * p::p] = False
-            mu[p::p] *= -1
-            mu[p * p::p * p] = 0
-    return mu
-
-
-def pi_D_closed_form(x: int) -> int:
-    """#{d <= x : d = 5 mod 8, d squarefree} by Moebius inversion over odd m:
-    sum_{m odd} mu(m) * #{n <= x/m^2 : n = 5 mod 8}   (m^2 = 1 mod 8)."""
-    M = isqrt(x)
-    mu = _mobius_upto(M)
-    tot = 0
-    for m in range(1, M + 1, 2):
-        if mu[m]:
-            tot += int(mu[m]) * ((x // (m * m) + 3) // 8)
-    return tot
-
-
 def test_pi_D_matches_mobius_closed_form():
     xs = [10, 100, 1000, 12345, 10**5, 10**6]
     f = C.classify_range(0, 10**6)
