@@ -3,6 +3,8 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cmath>
+#include <cstring>
 
 typedef uint64_t u64;
 typedef int64_t i64;
@@ -12,11 +14,67 @@ typedef uint8_t u8;
 
 #define FULL_MASK 0xffffffffu
 
+// Device step functions are also compiled for the host by the CPU emulation
+// harness in tests/ (tests/emu/kernel_emu.cu), which runs the same per-d state
+// machine lane by lane against the oracle.  The product library never calls
+// them on the host.
+#define EIS_HD __host__ __device__ __forceinline__
+
+// fast reciprocal: MUFU.RCP on the device; IEEE 1/x in the host emulation
+// (both are within the 2^-22 relative error the quotient proofs assume)
+EIS_HD float rcp_approx(float x) {
+#ifdef __CUDA_ARCH__
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return 1.0f / x;
+#endif
+}
+
+EIS_HD float u2f_bits(u32 v) {
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(v);
+#else
+    float f;
+    memcpy(&f, &v, 4);
+    return f;
+#endif
+}
+EIS_HD u32 f2u_bits(float f) {
+#ifdef __CUDA_ARCH__
+    return __float_as_uint(f);
+#else
+    u32 v;
+    memcpy(&v, &f, 4);
+    return v;
+#endif
+}
+
+// index of the lowest set bit (x != 0)
+EIS_HD int __builtin_ctz_portable(u32 x) {
+#ifdef __CUDA_ARCH__
+    return __ffs(x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+}
+
+EIS_HD float log2_approx(float x) {
+#ifdef __CUDA_ARCH__
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return log2f(x);
+#endif
+}
+
 // Candidate index i <-> d = 8 i + 5 (every d in D is = 5 mod 8).
 __host__ __device__ __forceinline__ u64 cand_d(u64 i) { return 8 * i + 5; }
 
 // floor(sqrt(d)) exactly for d < 2^53 (fp64 sqrt is within 1 ulp; two fixes).
-__device__ __forceinline__ u32 isqrt_u64_dev(u64 d) {
+EIS_HD u32 isqrt_u64_dev(u64 d) {
     u64 s = (u64)sqrt((double)d);
     while (s * s > d) --s;
     while ((s + 1) * (s + 1) <= d) ++s;

@@ -227,7 +227,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
                                      cudaGetErrorString(cudaGetLastError()));
         } else {
             const unsigned wblocks = (unsigned)(g.num_sms * g.blocks_per_sm);
-            walk_half_kernel<32><<<wblocks, 256, 0, s>>>(a);
+            walk_half_kernel<36><<<wblocks, 256, 0, s>>>(a);
             CUDA_TRY(cudaGetLastError());
             g.launches++;
         }

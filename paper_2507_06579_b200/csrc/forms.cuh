@@ -1,0 +1,250 @@
+// forms.cuh -- giant-step composition of the paper's Appendix:
+// NUCOMP (Alg. 2), NUDUPL (Alg. 3), NUCOMPchoose (Alg. 4) with the plain ideal
+// product for small norms, on binary quadratic forms (u, v, w) of discriminant d,
+// v^2 - 4uw = d.  Each returns the composed, near-reduced ideal [Q/2, (P+sqrt d)/2]
+// and the relative generator gamma (I = (1/gamma) I1 I2)
+// carried ONLY as
+//   * its residue t(gamma) in (O_K/2O_K)^* = Z/3, and
+//   * log2|gamma| (float; distances only choose the baby window and feed the
+//     trivial-match guard, R14/R29).
+// A, B, C of gamma = (A + B sqrt d)/C are never formed: with G odd (it divides
+// u1 = Q1/2), u3 odd and v3 odd, A + B sqrt d = 2G[(x u3 + y (v3-1)/2) + y w], C = 2 u3,
+// so t(gamma) = DLOG[(x + y (v3-1)/2) mod 2][y mod 2] (R12).  For the
+// plain product gamma = S is odd: t = 0.
+//
+// Integer widths: u1, u2 < 2^20 (reduced inputs); intermediates < 2^48 at
+// d <= 1e11, so int64 suffices; the plain-product numerator
+// uses __int128.
+#pragma once
+#include "common.cuh"
+
+EIS_HD i64 floor_div(i64 a, i64 b) {   // b > 0
+    i64 q = a / b;
+    return (a % b != 0 && a < 0) ? q - 1 : q;
+}
+EIS_HD i64 floor_mod(i64 a, i64 b) {   // b > 0, result in [0, b)
+    i64 r = a % b;
+    return r < 0 ? r + b : r;
+}
+EIS_HD i64 iabs64(i64 a) { return a < 0 ? -a : a; }
+
+// Extended Euclid for a, b >= 0: returns g = gcd(a, b) = x a + y b.
+EIS_HD i64 xgcd(i64 a, i64 b, i64 &x, i64 &y) {
+    i64 x0 = 1, y0 = 0, x1 = 0, y1 = 1;
+    while (b != 0) {
+        i64 q;
+        if (a < 0x7fffffff && b < 0x7fffffff) q = (i64)((u32)a / (u32)b);
+        else q = a / b;
+        i64 t = a - q * b; a = b; b = t;
+        t = x0 - q * x1; x0 = x1; x1 = t;
+        t = y0 - q * y1; y0 = y1; y1 = t;
+    }
+    x = x0;
+    y = y0;
+    return a;
+}
+// signed variant: g = gcd(|a|, |b|) = x a + y b
+EIS_HD i64 xgcd_s(i64 a, i64 b, i64 &x, i64 &y) {
+    i64 g = xgcd(iabs64(a), iabs64(b), x, y);
+    if (a < 0) x = -x;
+    if (b < 0) y = -y;
+    return g;
+}
+
+// Exact division (the "without remainder" divisions of Algs. 2-3); *err++ if not exact.
+EIS_HD i64 exact_div(i64 n, i64 dv, u32 *err) {
+    i64 q = n / dv;
+    if (q * dv != n) *err += 1;
+    return q;
+}
+
+struct Composed {
+    i64 Q, P;      // the ideal [Q/2, (P + sqrt d)/2], Q > 0 (not necessarily reduced)
+    u32 tg;        // t(gamma) in {0,1,2}
+    float lg;      // log2 |gamma|
+    u32 kind;      // 0 plain product, 1 NUCOMP, 2 NUDUPL
+};
+
+// residue of gamma from the final Euclid cofactors (R12)
+EIS_HD u32 t_gamma(i64 x, i64 y, i64 v3) {
+    const u32 a = (u32)((x + (y * ((v3 - 1) >> 1))) & 1);
+    const u32 b = (u32)(y & 1);
+    return a ? (b ? 2u : 0u) : 1u;    // (1,0)->0, (0,1)->1, (1,1)->2; (0,0) impossible
+}
+
+// log2|gamma|, gamma = G (a + y sqrt d)/(2 u3), a = 2 x u3 + y v3.  If a and y
+// have opposite signs the sum cancels; then use |N(gamma)| = (Q1/2)(Q2/2)/|u3|
+// (norms of the ideals, R29) and the conjugate, which does not cancel.
+EIS_HD float log2_gamma(i64 G, i64 x, i64 y, i64 u3, i64 v3, double sqrtd, i64 Q1, i64 Q2) {
+    const i64 a = 2 * x * u3 + y * v3;
+    const double mag = fabs((double)a) + fabs((double)y) * sqrtd;   // |a| + |y| sqrt d
+    const float lconj = log2_approx((float)G) + log2_approx((float)mag) -
+                        log2_approx((float)iabs64(2 * u3));
+    if ((a >= 0) == (y >= 0) || a == 0 || y == 0) return lconj;  // no cancellation
+    const float lnorm = log2_approx((float)(Q1 >> 1)) + log2_approx((float)(Q2 >> 1)) -
+                        log2_approx((float)iabs64(u3));
+    return lnorm - lconj;
+}
+
+// Partial Euclid of Algs. 2-3.
+EIS_HD void partial_euclid(i64 &bx, i64 &by, i64 &x, i64 &y, int &z, i64 L) {
+    x = 1; y = 0; z = 0;
+    while (iabs64(by) > L && bx != 0) {
+        i64 q;
+        if (bx < 0x7fffffff && by < 0x7fffffff && bx > 0 && by > 0) q = (i64)((u32)by / (u32)bx);
+        else q = by / bx;
+        i64 t = by - q * bx;
+        by = bx; bx = t;
+        t = y - q * x;
+        y = x; x = t;
+        z++;
+    }
+    if (z & 1) { by = -by; y = -y; }
+}
+
+// Algorithm 2 NUCOMP on forms (u1,v1,w1), (u2,v2,w2).
+EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u3, i64 &v3,
+                   i64 &w3, i64 &G, i64 &xo, i64 &yo, u32 *err) {
+    if (w1 < w2) {
+        i64 t;
+        t = u1; u1 = u2; u2 = t;
+        t = v1; v1 = v2; v2 = t;
+        t = w1; w1 = w2; w2 = t;
+    }
+    const i64 s = (v1 + v2) / 2;    // exact: v1, v2 odd
+    const i64 m = v2 - s;
+    i64 b, c;
+    const i64 F = xgcd(u2, u1, b, c);   // b u2 + c u1 = F
+    i64 Bx, By, Cy, Dy;
+    if (s % F == 0) {
+        G = F;
+        Bx = m * b;
+        By = u1 / G;
+        Cy = u2 / G;
+        Dy = s / G;
+    } else {
+        i64 xx, yy;
+        G = xgcd_s(F, s, xx, yy);       // xx F + yy s = G
+        const i64 H = F / G;
+        By = u1 / G;
+        Cy = u2 / G;
+        Dy = s / G;
+        const i64 inner = floor_mod(b * floor_mod(w1, H) + c * floor_mod(w2, H), H);
+        const i64 l = floor_mod(floor_mod(yy, H) * inner, H);
+        Bx = exact_div(b * m + l * By, H, err);
+    }
+    i64 bx = floor_mod(Bx, By), by = By, x, y;
+    int z;
+    partial_euclid(bx, by, x, y, z, L);
+    const i64 ax = G * x, ay = G * y;
+    if (z != 0) {
+        const i64 cx = exact_div(Cy * bx - m * x, By, err);
+        const i64 Q1 = by * cx;
+        const i64 Q2 = Q1 + m;
+        const i64 dx = exact_div(Dy * bx - w2 * x, By, err);
+        const i64 Q3 = y * dx;
+        const i64 Q4 = Q3 + Dy;
+        const i64 dy = exact_div(Q4, x, err);
+        i64 cy;
+        if (bx != 0) cy = exact_div(Q2, bx, err);
+        else cy = exact_div(cx * dy - w1, dx, err);
+        u3 = by * cy - ay * dy;
+        w3 = bx * cx - ax * dx;
+        v3 = G * (Q3 + Q4) - Q1 - Q2;
+    } else {
+        const i64 Q1 = Cy * bx;
+        const i64 cx = exact_div(Q1 - m, By, err);
+        const i64 dx = exact_div(bx * Dy - w2, By, err);
+        u3 = by * Cy;
+        w3 = bx * cx - G * dx;
+        v3 = v2 - 2 * Q1;
+    }
+    xo = x;
+    yo = y;
+}
+
+// Algorithm 3 NUDUPL on the form (u, v, w).
+EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &w3, i64 &G, i64 &xo,
+                   i64 &yo, u32 *err) {
+    i64 xx, yy;
+    G = xgcd_s(u, v, xx, yy);     // xx u + yy v = G
+    const i64 By = u / G;
+    const i64 Dy = v / G;
+    const i64 Bx = floor_mod(floor_mod(yy, By) * floor_mod(w, By), By);
+    i64 bx = Bx, by = By, x, y;
+    int z;
+    partial_euclid(bx, by, x, y, z, L);
+    const i64 ax = G * x, ay = G * y;
+    if (z == 0) {
+        const i64 dx = exact_div(bx * Dy - w, By, err);
+        u3 = by * by;
+        w3 = bx * bx;
+        v3 = v - (bx + by) * (bx + by) + u3 + w3;
+        w3 = w3 - G * dx;
+    } else {
+        const i64 dx = exact_div(bx * Dy - w * x, By, err);
+        const i64 Q1 = dx * y;
+        i64 dy = Q1 + Dy;
+        v3 = G * (dy + Q1);
+        dy = exact_div(dy, x, err);
+        u3 = by * by;
+        w3 = bx * bx;
+        v3 = v3 - (bx + by) * (bx + by) + u3 + w3;
+        u3 = u3 - ay * dy;
+        w3 = w3 - ax * dx;
+    }
+    xo = x;
+    yo = y;
+}
+
+// Plain ideal product (the small-norm branch of Alg. 4, PAPER.md l.733, l.742-744;
+// the J-W Sec. 5.4 procedure is not reproduced in the paper: Dirichlet
+// composition, R20).  Inputs a_i = Q_i/2, b_i = P_i (odd).
+EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
+    const i64 a1 = Q1 >> 1, a2 = Q2 >> 1;
+    i64 x, y;
+    const i64 e = xgcd(a1, a2, x, y);         // x a1 + y a2 = e
+    const i64 n = (P1 + P2) / 2;
+    i64 X, Y;
+    const i64 S = xgcd_s(e, n, X, Y);         // X e + Y n = S
+    const i64 a3 = (a1 / S) * (a2 / S);
+    const __int128 num = (__int128)X * x * a1 * P2 + (__int128)X * y * a2 * P1 +
+                         (__int128)Y * (((__int128)P1 * P2 + d) / 2);
+    if (num % S != 0) *err += 1;
+    const __int128 M = 2 * (__int128)a3;
+    __int128 b3 = (num / S) % M;
+    if (b3 < 0) b3 += M;
+    Composed r;
+    r.Q = 2 * a3;
+    r.P = (i64)b3;
+    r.tg = 0;                                  // gamma = S odd
+    r.lg = log2_approx((float)S);
+    r.kind = 0;
+    return r;
+}
+
+// Algorithm 4 NUCOMPchoose for reduced ideals
+// I1 = [Q1/2, (P1+sqrt d)/2], I2 = [Q2/2, (P2+sqrt d)/2].
+EIS_HD Composed nucomp_choose(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, i64 L, double sqrtd,
+                              int plain_th, u32 *err) {
+    P1 = floor_mod(P1, Q1);
+    P2 = floor_mod(P2, Q2);
+    if (Q1 <= plain_th || Q2 <= plain_th) return plain_product(Q1, P1, Q2, P2, d, err);
+    const i64 w1 = exact_div(P1 * P1 - d, 2 * Q1, err);
+    i64 u3, v3, w3, G, x, y;
+    Composed r;
+    if (Q1 == Q2 && P1 == P2) {
+        nudupl(Q1 >> 1, -P1, w1, L, u3, v3, w3, G, x, y, err);
+        r.kind = 2;
+    } else {
+        const i64 w2 = exact_div(P2 * P2 - d, 2 * Q2, err);
+        nucomp(Q1 >> 1, -P1, w1, Q2 >> 1, -P2, w2, L, u3, v3, w3, G, x, y, err);
+        r.kind = 1;
+    }
+    r.Q = iabs64(2 * u3);
+    r.P = floor_mod(-v3, r.Q);
+    r.tg = t_gamma(x, y, v3);
+    r.lg = log2_gamma(G, x, y, u3, v3, sqrtd, Q1, Q2);
+    if ((r.Q & 3) != 2 || (r.P & 1) != 1 || (G & 1) == 0) *err += 1;   // Thm A.1 / 2 inert
+    return r;
+}

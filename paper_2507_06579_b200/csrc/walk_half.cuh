@@ -27,48 +27,60 @@
 
 struct BabyState {
     u32 s, P, Q, Qp;   // isqrt(d), P_j, Q_j, Q_{j-1}
-    u32 m, b;          // steps done, sum of bit1(P) over them: t(theta_{m+1}) = m + b
+    u32 t2;            // 2 t(theta_{j+1}) (not reduced mod 3)
 };
 
-__device__ __forceinline__ void baby_init(BabyState &st, u64 d) {
-    st.s = isqrt_u64_dev(d);
-    st.P = 1;
-    st.Q = 2;
-    st.Qp = (u32)((d - 1) >> 1);   // Q_{-1} = (d - P_0^2)/Q_0, mod 2^32
-    st.m = 0;
-    st.b = 0;
+// First rho step in closed form (PAPER.md l.541 from (Q_0, P_0) = (2, 1)):
+// q_0 = floor((1 + s)/2), P_1 = 2 q_0 - 1 = s or s - 1 (the odd one),
+// Q_1 = (d - P_1^2)/2, t(theta_2) = 1 + bit1(P_1).  The symmetry test at
+// j = 1 is Q_1 = Q_0 = 2 only (the P test needs j >= 2).  Returns true with
+// *res = t(eps) = t(theta_1) + t(theta_2) if the walk already ends here.
+EIS_HD bool baby_init(BabyState &st, u64 d, u32 *res) {
+    const u32 s = isqrt_u64_dev(d);
+    const u32 P1 = (s - 1) | 1u;
+    const u32 Q1 = (u32)((d - (u64)P1 * P1) >> 1);
+    st.s = s;
+    st.P = P1;
+    st.Q = Q1;
+    st.Qp = 2;
+    st.t2 = 2 + (P1 & 2);
+    *res = st.t2 >> 1;
+    return Q1 == 2;
 }
 
-__device__ __forceinline__ float u32_to_f_exact(u32 v) {   // v < 2^23
-    return __int_as_float((int)(v | 0x4B000000u)) - 8388608.0f;
+EIS_HD float u32_to_f_exact(u32 v) {   // v < 2^23
+    return u2f_bits(v | 0x4B000000u) - 8388608.0f;
 }
 
-// One rho step.  Returns true at the symmetry point with *res = t(eps) (not reduced mod 3).
-__device__ __forceinline__ bool baby_step(BabyState &st, u32 *res) {
+// One rho step j >= 2 from (Q_{j-1}, P_{j-1}) = (st.Q, st.P) with Q_{j-2} = st.Qp.
+// Returns true at the symmetry point (Q_j = Q_{j-1} or P_j = P_{j-1}); the
+// state is then already advanced and baby_result() reads t(eps) from it.
+EIS_HD bool baby_step(BabyState &st) {
     const u32 num = st.P + st.s;
     const float nf = u32_to_f_exact(num);
-    const float qf = u32_to_f_exact(st.Q);
-    float rq;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"(qf));
-    u32 q = __float_as_uint(fmaf(nf, rq, 8388608.0f)) - 0x4B000000u;   // round(num/Q)
-    i32 r = (i32)(num - q * st.Q);
-    if (r < 0) { q -= 1; r += (i32)st.Q; }
-    const u32 Pn = st.s - (u32)r;
-    const u32 Qn = st.Qp + q * (st.P - Pn);
-    const u32 bit = (Pn >> 1) & 1u;
-    const u32 tc = st.m + st.b;               // t(theta_j)
-    const bool exQ = (Qn == st.Q);
-    const bool exP = (Pn == st.P) && (st.m >= 1);
-    st.m += 1;
-    st.b += bit;
+    const float rq = rcp_approx(u32_to_f_exact(st.Q));
+    // -q0 with q0 = round(num/Q) in {floor, floor + 1}  (|num/Q - num*rq| < 0.27)
+    const u32 nq0 = 0x4B000000u - f2u_bits(fmaf(nf, rq, 8388608.0f));
+    const i32 r0 = (i32)(nq0 * st.Q + num);                 // num - q0 Q in [-Q, Q)
+    const u32 m = (u32)(r0 >> 31);                          // all ones iff q0 = floor + 1
+    const u32 Pn = st.s - (u32)r0 - (st.Q & m);             // P_j = s - (num mod Q)
+    const u32 q = m - nq0;                                  // q_{j-1} = floor(num/Q)
+    const u32 Qn = st.Qp + q * (st.P - Pn);                 // Q_j (wrapping u32, exact)
+    st.t2 += (Pn & 2u) + 2u;                                // residue of (P_j + sqrt d)/Q_{j-1}
+    const bool eP = (Pn == st.P);
     st.Qp = st.Q;
     st.Q = Qn;
     st.P = Pn;
-    if (exQ | exP) {
-        *res = exQ ? (2 * tc + 1 + bit) : 2 * tc;
-        return true;
-    }
-    return false;
+    return (Qn == st.Qp) | eP;
+}
+
+// t(eps) (not reduced mod 3) at the symmetry point reached by baby_step
+// (R7):
+//   Q_j = Q_{j-1}:  t(theta_j) + t(theta_{j+1});   P_j = P_{j-1}:  2 t(theta_j).
+EIS_HD u32 baby_result(const BabyState &st) {
+    const u32 inc = (st.P & 2u) + 2u;        // 2 (t(theta_{j+1}) - t(theta_j))
+    const u32 t2b = st.t2 - inc;             // 2 t(theta_j)
+    return (st.Q == st.Qp) ? (st.t2 + t2b) >> 1 : t2b;
 }
 
 template <int KSTEPS>
@@ -86,6 +98,18 @@ walk_half_kernel(WalkArgs a) {
     bool active = false, exhausted = false;
     u32 n_done = 0, n_sym = 0;
     u64 steps = 0;
+    auto finish = [&](u32 res) {
+        const u32 t = res % 3;
+        steps += 1;                       // the closed-form first step
+        n_done++;
+        n_sym++;
+        if (a.flags) a.flags[off] = (u8)t;
+        if (a.ckpt) {
+            const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
+            atomicAdd(&hist[b], 1u);
+            if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
+        }
+    };
 
     for (;;) {
         const u32 need = __ballot_sync(FULL_MASK, !active && !exhausted);
@@ -99,8 +123,12 @@ walk_half_kernel(WalkArgs a) {
                 if (idx < n) {
                     off = __ldg(a.list + idx);
                     d = cand_d(a.i0 + off);
-                    baby_init(st, d);
-                    active = true;
+                    u32 r1;
+                    if (baby_init(st, d, &r1)) {
+                        finish(r1);            // period closes at j = 1 (d = P_1^2 + 4)
+                    } else {
+                        active = true;
+                    }
                 } else {
                     exhausted = true;
                 }
@@ -108,23 +136,15 @@ walk_half_kernel(WalkArgs a) {
         }
         if (__all_sync(FULL_MASK, exhausted)) break;
         if (active) {
-            u32 res = 0;
             bool fin = false;
-#pragma unroll 4
-            for (int k = 0; k < KSTEPS; k++) {
-                if (baby_step(st, &res)) { fin = true; break; }
+            int k = 0;
+#pragma unroll 6
+            for (; k < KSTEPS; k++) {
+                if (baby_step(st)) { fin = true; break; }
             }
+            steps += (u32)(k + fin);
             if (fin) {
-                const u32 t = res % 3;
-                steps += st.m;
-                n_done++;
-                n_sym++;
-                if (a.flags) a.flags[off] = (u8)t;
-                if (a.ckpt) {
-                    const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
-                    atomicAdd(&hist[b], 1u);
-                    if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
-                }
+                finish(baby_result(st));
                 active = false;
             }
         }

@@ -1,0 +1,78 @@
+// kernel_emu.cu -- TEST HARNESS: runs the walk kernels' per-lane state machines
+// (the __host__ __device__ functions of walk_half.cuh / walk_bsgs.cuh) on the
+// CPU, one d at a time, so their arithmetic can be checked against the oracle
+// without a GPU.  Not part of the product library.
+//
+// usage: kernel_emu MODE ALPHA_X16 NS_LOG2 < d-list     (MODE: half | bsgs)
+// prints per d: "d t baby giant reduce fallback err kinds(plain,comp,dupl)"
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../paper_2507_06579_b200/csrc/walk_bsgs.cuh"
+
+int main(int argc, char **argv) {
+    if (argc < 4) {
+        fprintf(stderr, "usage: %s half|bsgs alpha_x16 ns_log2(0=auto)\n", argv[0]);
+        return 2;
+    }
+    const bool bsgs = strcmp(argv[1], "bsgs") == 0;
+    BsgsArgs B;
+    B.alpha = atoi(argv[2]) / 16.0f;
+    const int ns_fixed = atoi(argv[3]);
+    B.plain_th = argc > 4 ? atoi(argv[4]) : 50;
+    B.giant_cap_mul = 20.0f;
+    std::vector<u32> bm(1 << 10);
+    std::vector<u64> tab(1 << 14);
+    unsigned long long d;
+    while (scanf("%llu", &d) == 1) {
+        u32 res = 0, err = 0;
+        u64 baby = 0, giant = 0, red = 0, fb = 0, kinds[3] = {0, 0, 0};
+        if (!bsgs) {
+            BabyState st;
+            u32 r1;
+            baby = 1;
+            if (baby_init(st, d, &r1)) res = r1;
+            else {
+                for (;;) { baby++; if (baby_step(st)) break; }
+                res = baby_result(st);
+            }
+        } else {
+            B.ns_log2 = ns_fixed ? ns_fixed : bsgs_ns_log2(d, B.alpha);
+            B.cap = (1 << B.ns_log2) / 2 - 2;
+            Store S;
+            S.bm = bm.data();
+            S.stride = 1;
+            S.tab = tab.data();
+            S.ns_log2 = B.ns_log2;
+            BsgsLane ln;
+            baby = 1;
+            bsgs_begin(ln, S, B, d);
+            while (ln.phase != PH_DONE) {
+                if (ln.phase == PH_BABY) baby += bsgs_baby(ln, S, B, 8);
+                if (ln.phase == PH_GIANT) {
+                    GiantInfo gi = bsgs_giant(ln, S, B, &err);
+                    giant++;
+                    red += gi.nred;
+                    kinds[gi.kind]++;
+                    if (ln.phase == PH_HALF) {
+                        fb++;
+                        u32 r1;
+                        if (baby_init(ln.st, ln.d, &r1)) { ln.res = r1; ln.phase = PH_DONE; }
+                    }
+                }
+                if (ln.phase == PH_HALF) {
+                    baby++;
+                    if (baby_step(ln.st)) { ln.res = baby_result(ln.st); ln.phase = PH_DONE; }
+                }
+            }
+            res = ln.res;
+        }
+        printf("%llu %u %llu %llu %llu %llu %u %llu %llu %llu\n", d, res % 3,
+               (unsigned long long)baby, (unsigned long long)giant, (unsigned long long)red,
+               (unsigned long long)fb, err, (unsigned long long)kinds[0],
+               (unsigned long long)kinds[1], (unsigned long long)kinds[2]);
+    }
+    return 0;
+}

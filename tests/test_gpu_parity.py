@@ -20,7 +20,7 @@ from pins import paper_windows, pi_D_closed_form
 
 pytestmark = pytest.mark.gpu
 
-MODES = {"half": eis.MODE_HALF, "auto": eis.MODE_AUTO}
+MODES = {"half": eis.MODE_HALF, "bsgs": eis.MODE_BSGS, "auto": eis.MODE_AUTO}
 NTHREADS = 0   # oracle: all host cores
 
 
