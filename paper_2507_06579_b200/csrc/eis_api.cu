@@ -171,8 +171,17 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
               int n, u64 *buckets_dev, cudaStream_t s) {
     const u64 SEG = 1ull << g.segment_log2;
     const int n_small = primes_small();
+    // BSGS keeps one store per survivor of the segment: cap the segment so the
+    // stores stay within ~16 GB of HBM.
+    const bool bsgs = want_bsgs(cand_d(i_first));
+    u64 seg_cap = SEG;
+    if (bsgs) {
+        const int nsl = bsgs_ns_log2(cand_d(i_last), g.alpha_x16 / 16.0f);
+        const u64 per = ((u64)8 << nsl) + ((u64)4 << nsl) / 32 + sizeof(GiantRec) + 4;
+        seg_cap = std::min<u64>(SEG, std::max<u64>((16ull << 30) / per, 1ull << 16));
+    }
     for (u64 seg = i_first; seg <= i_last;) {
-        u64 len = std::min(SEG, i_last - seg + 1);
+        u64 len = std::min(seg_cap, i_last - seg + 1);
         int b_lo = 0, nb = 0;
         if (x_host) {
             // bucket span of [d(seg), d(seg+len-1)] must fit HIST_CAP
@@ -219,9 +228,9 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.buckets = buckets_dev;
         a.stats = g.d_stats;
         CUDA_TRY(cudaEventRecord(g.ev[2], s));
-        if (want_bsgs(cand_d(seg))) {
-            int rc = launch_bsgs(a, cand_d(seg), d_last, g.num_sms, g.alpha_x16, g.bsgs,
-                                 g.d_ctr + 3, s, &g.launches);
+        if (bsgs) {
+            int rc = launch_bsgs(a, len, d_last, g.num_sms, g.alpha_x16, g.bsgs, g.d_ctr + 3, s,
+                                 &g.launches);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS launch failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -359,7 +368,7 @@ int eis_set_option(const char *key, int64_t v) {
         if (v < 0) return fail(EIS_EINVAL, "crossover must be >= 0");
         g.crossover = (u64)v;
     } else if (k == "alpha_x16") {
-        if (v < 4 || v > 256) return fail(EIS_EINVAL, "alpha_x16 must be in [4, 256]");
+        if (v < 4 || v > 64) return fail(EIS_EINVAL, "alpha_x16 must be in [4, 64]");
         g.alpha_x16 = (int)v;
     } else if (k == "segment_log2") {
         if (v < 18 || v > 31) return fail(EIS_EINVAL, "segment_log2 must be in [18, 31]");

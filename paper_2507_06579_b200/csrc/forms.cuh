@@ -18,30 +18,70 @@
 #pragma once
 #include "common.cuh"
 
-EIS_HD i64 floor_div(i64 a, i64 b) {   // b > 0
-    i64 q = a / b;
-    return (a % b != 0 && a < 0) ? q - 1 : q;
-}
-EIS_HD i64 floor_mod(i64 a, i64 b) {   // b > 0, result in [0, b)
-    i64 r = a % b;
-    return r < 0 ? r + b : r;
-}
 EIS_HD i64 iabs64(i64 a) { return a < 0 ? -a : a; }
 
-// Extended Euclid for a, b >= 0: returns g = gcd(a, b) = x a + y b.
-EIS_HD i64 xgcd(i64 a, i64 b, i64 &x, i64 &y) {
-    i64 x0 = 1, y0 = 0, x1 = 0, y1 = 1;
+// ---- division helpers (no 64-bit integer divide instruction exists; nvcc's
+// i64 '/' is a ~100-instruction branchy routine).  All divisors here are
+// < 2^32 and all quotients < 2^50 (K3-giant).
+
+// 1/b to full double precision: MUFU.RCP64H seed + two Newton steps.
+EIS_HD double rcp64(double b) {
+#ifdef __CUDA_ARCH__
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    double e = fma(-b, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-b, r, 1.0);
+    r = fma(r, e, r);
+    return r;
+#else
+    return 1.0 / b;
+#endif
+}
+
+// floor(a / b) for b > 0, |a| < 2^62, |a/b| < 2^50: double estimate, one
+// integer correction each way.
+EIS_HD i64 floor_div(i64 a, i64 b) {
+    i64 q = (i64)floor((double)a * rcp64((double)b));
+    i64 r = a - q * b;
+    if (r < 0) { q -= 1; r += b; }
+    if (r >= b) { q += 1; }
+    return q;
+}
+EIS_HD i64 floor_mod(i64 a, i64 b) {   // b > 0, result in [0, b)
+    return a - floor_div(a, b) * b;
+}
+
+// 32-bit floor division for 0 <= a < 2^23, 0 < b < 2^23 (same float trick as
+// the baby step: round(a/b) by one FFMA, then one correction).
+EIS_HD u32 udiv23(u32 a, u32 b) {
+    const float af = u2f_bits(a | 0x4B000000u) - 8388608.0f;
+    const float rb = rcp_approx(u2f_bits(b | 0x4B000000u) - 8388608.0f);
+    u32 q = f2u_bits(fmaf(af, rb, 8388608.0f)) - 0x4B000000u;
+    if ((i32)(a - q * b) < 0) q -= 1;
+    return q;
+}
+
+// Extended Euclid for 0 <= a, b < 2^23: returns g = gcd(a, b) = x a + y b
+// (|x|, |y| <= max(a, b), so 32-bit cofactors suffice).
+EIS_HD i32 xgcd32(i32 a, i32 b, i32 &x, i32 &y) {
+    i32 x0 = 1, y0 = 0, x1 = 0, y1 = 1;
     while (b != 0) {
-        i64 q;
-        if (a < 0x7fffffff && b < 0x7fffffff) q = (i64)((u32)a / (u32)b);
-        else q = a / b;
-        i64 t = a - q * b; a = b; b = t;
+        const i32 q = (i32)udiv23((u32)a, (u32)b);
+        i32 t = a - q * b; a = b; b = t;
         t = x0 - q * x1; x0 = x1; x1 = t;
         t = y0 - q * y1; y0 = y1; y1 = t;
     }
     x = x0;
     y = y0;
     return a;
+}
+EIS_HD i64 xgcd(i64 a, i64 b, i64 &x, i64 &y) {   // a, b in [0, 2^23)
+    i32 xx, yy;
+    const i32 g = xgcd32((i32)a, (i32)b, xx, yy);
+    x = xx;
+    y = yy;
+    return g;
 }
 // signed variant: g = gcd(|a|, |b|) = x a + y b
 EIS_HD i64 xgcd_s(i64 a, i64 b, i64 &x, i64 &y) {
@@ -51,11 +91,26 @@ EIS_HD i64 xgcd_s(i64 a, i64 b, i64 &x, i64 &y) {
     return g;
 }
 
-// Exact division (the "without remainder" divisions of Algs. 2-3); *err++ if not exact.
-EIS_HD i64 exact_div(i64 n, i64 dv, u32 *err) {
-    i64 q = n / dv;
+// exact division of small integers: |a| < 2^23, 0 < b < 2^23, b | a
+EIS_HD i64 sdiv_exact23(i64 a, i64 b) {
+    const u32 q = udiv23((u32)iabs64(a), (u32)b);
+    return a < 0 ? -(i64)q : (i64)q;
+}
+// does b divide a?  |a| < 2^23, 0 < b < 2^23
+EIS_HD bool divides23(i64 b, i64 a) {
+    const u32 ua = (u32)iabs64(a);
+    return ua - udiv23(ua, (u32)b) * (u32)b == 0;
+}
+
+// Exact division (the "without remainder" divisions of Algs. 2-3), |n/dv| < 2^50:
+// the rounded double quotient is exact; *err++ if the remainder is not 0.
+EIS_HD i64 exact_div_r(i64 n, i64 dv, double rdv, u32 *err) {
+    const i64 q = (i64)rint((double)n * rdv);
     if (q * dv != n) *err += 1;
     return q;
+}
+EIS_HD i64 exact_div(i64 n, i64 dv, u32 *err) {
+    return exact_div_r(n, dv, rcp64((double)dv), err);
 }
 
 struct Composed {
@@ -88,18 +143,19 @@ EIS_HD float log2_gamma(i64 G, i64 x, i64 y, i64 u3, i64 v3, double sqrtd, i64 Q
 
 // Partial Euclid of Algs. 2-3.
 EIS_HD void partial_euclid(i64 &bx, i64 &by, i64 &x, i64 &y, int &z, i64 L) {
-    x = 1; y = 0; z = 0;
-    while (iabs64(by) > L && bx != 0) {
-        i64 q;
-        if (bx < 0x7fffffff && by < 0x7fffffff && bx > 0 && by > 0) q = (i64)((u32)by / (u32)bx);
-        else q = by / bx;
-        i64 t = by - q * bx;
-        by = bx; bx = t;
-        t = y - q * x;
-        y = x; x = t;
+    // 0 <= bx < by < 2^23 on entry (bx = Bx mod By, By = u1/G)
+    i32 bx32 = (i32)bx, by32 = (i32)by, x32 = 1, y32 = 0;
+    z = 0;
+    while (by32 > L && bx32 != 0) {
+        const i32 q = (i32)udiv23((u32)by32, (u32)bx32);
+        i32 t = by32 - q * bx32;
+        by32 = bx32; bx32 = t;
+        t = y32 - q * x32;
+        y32 = x32; x32 = t;
         z++;
     }
-    if (z & 1) { by = -by; y = -y; }
+    if (z & 1) { by32 = -by32; y32 = -y32; }
+    bx = bx32; by = by32; x = x32; y = y32;
 }
 
 // Algorithm 2 NUCOMP on forms (u1,v1,w1), (u2,v2,w2).
@@ -116,19 +172,19 @@ EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u
     i64 b, c;
     const i64 F = xgcd(u2, u1, b, c);   // b u2 + c u1 = F
     i64 Bx, By, Cy, Dy;
-    if (s % F == 0) {
+    if (divides23(F, s)) {
         G = F;
         Bx = m * b;
-        By = u1 / G;
-        Cy = u2 / G;
-        Dy = s / G;
+        By = sdiv_exact23(u1, G);
+        Cy = sdiv_exact23(u2, G);
+        Dy = sdiv_exact23(s, G);
     } else {
         i64 xx, yy;
         G = xgcd_s(F, s, xx, yy);       // xx F + yy s = G
-        const i64 H = F / G;
-        By = u1 / G;
-        Cy = u2 / G;
-        Dy = s / G;
+        const i64 H = sdiv_exact23(F, G);
+        By = sdiv_exact23(u1, G);
+        Cy = sdiv_exact23(u2, G);
+        Dy = sdiv_exact23(s, G);
         const i64 inner = floor_mod(b * floor_mod(w1, H) + c * floor_mod(w2, H), H);
         const i64 l = floor_mod(floor_mod(yy, H) * inner, H);
         Bx = exact_div(b * m + l * By, H, err);
@@ -138,10 +194,11 @@ EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u
     partial_euclid(bx, by, x, y, z, L);
     const i64 ax = G * x, ay = G * y;
     if (z != 0) {
-        const i64 cx = exact_div(Cy * bx - m * x, By, err);
+        const double rBy = rcp64((double)By);
+        const i64 cx = exact_div_r(Cy * bx - m * x, By, rBy, err);
         const i64 Q1 = by * cx;
         const i64 Q2 = Q1 + m;
-        const i64 dx = exact_div(Dy * bx - w2 * x, By, err);
+        const i64 dx = exact_div_r(Dy * bx - w2 * x, By, rBy, err);
         const i64 Q3 = y * dx;
         const i64 Q4 = Q3 + Dy;
         const i64 dy = exact_div(Q4, x, err);
@@ -152,9 +209,10 @@ EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u
         w3 = bx * cx - ax * dx;
         v3 = G * (Q3 + Q4) - Q1 - Q2;
     } else {
+        const double rBy = rcp64((double)By);
         const i64 Q1 = Cy * bx;
-        const i64 cx = exact_div(Q1 - m, By, err);
-        const i64 dx = exact_div(bx * Dy - w2, By, err);
+        const i64 cx = exact_div_r(Q1 - m, By, rBy, err);
+        const i64 dx = exact_div_r(bx * Dy - w2, By, rBy, err);
         u3 = by * Cy;
         w3 = bx * cx - G * dx;
         v3 = v2 - 2 * Q1;
@@ -168,8 +226,8 @@ EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &w3, i64 &G
                    i64 &yo, u32 *err) {
     i64 xx, yy;
     G = xgcd_s(u, v, xx, yy);     // xx u + yy v = G
-    const i64 By = u / G;
-    const i64 Dy = v / G;
+    const i64 By = sdiv_exact23(u, G);
+    const i64 Dy = sdiv_exact23(v, G);
     const i64 Bx = floor_mod(floor_mod(yy, By) * floor_mod(w, By), By);
     i64 bx = Bx, by = By, x, y;
     int z;
@@ -223,22 +281,34 @@ EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
     return r;
 }
 
+// The fixed left operand of every giant step (mu_1), normalised as in Alg. 4
+// (P mod Q, w = (P^2 - d)/(2Q)) once per d.
+struct Mu1Form {
+    i64 Q, P, w;
+};
+EIS_HD Mu1Form mu1_form(i64 Q1, i64 P1, i64 d, u32 *err) {
+    Mu1Form f;
+    f.Q = Q1;
+    f.P = floor_mod(P1, Q1);
+    f.w = exact_div(f.P * f.P - d, 2 * Q1, err);
+    return f;
+}
+
 // Algorithm 4 NUCOMPchoose for reduced ideals
-// I1 = [Q1/2, (P1+sqrt d)/2], I2 = [Q2/2, (P2+sqrt d)/2].
-EIS_HD Composed nucomp_choose(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, i64 L, double sqrtd,
+// I1 = mu_1 = [Q1/2, (P1+sqrt d)/2] (pre-normalised) and I2 = [Q2/2, (P2+sqrt d)/2].
+EIS_HD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 L, double sqrtd,
                               int plain_th, u32 *err) {
-    P1 = floor_mod(P1, Q1);
-    P2 = floor_mod(P2, Q2);
+    const i64 Q1 = m1.Q, P1 = m1.P;
+    P2 = P2 < Q2 ? P2 : floor_mod(P2, Q2);
     if (Q1 <= plain_th || Q2 <= plain_th) return plain_product(Q1, P1, Q2, P2, d, err);
-    const i64 w1 = exact_div(P1 * P1 - d, 2 * Q1, err);
     i64 u3, v3, w3, G, x, y;
     Composed r;
     if (Q1 == Q2 && P1 == P2) {
-        nudupl(Q1 >> 1, -P1, w1, L, u3, v3, w3, G, x, y, err);
+        nudupl(Q1 >> 1, -P1, m1.w, L, u3, v3, w3, G, x, y, err);
         r.kind = 2;
     } else {
         const i64 w2 = exact_div(P2 * P2 - d, 2 * Q2, err);
-        nucomp(Q1 >> 1, -P1, w1, Q2 >> 1, -P2, w2, L, u3, v3, w3, G, x, y, err);
+        nucomp(Q1 >> 1, -P1, m1.w, Q2 >> 1, -P2, w2, L, u3, v3, w3, G, x, y, err);
         r.kind = 1;
     }
     r.Q = iabs64(2 * u3);

@@ -1,7 +1,16 @@
 // walk_bsgs.cuh -- K3 in BSGS mode: the paper's Algorithm 1
 // with residues in Z/3 (l.585-603): baby steps rho into a per-d store, then
 // giant steps mu_k = mu_1 * mu'_{k-1} by NUCOMPchoose (forms.cuh), rho-reduction,
-// and a store lookup.  One lane per d, persistent CTAs, warp-aggregated refill.
+// and a store lookup.
+//
+// Two kernels per segment (phase-pure warps; a fused kernel measured 9/32 warp
+// efficiency, K3-giant):
+//   bsgs_baby_kernel   warp-synchronous batches of 32 d: bsgs_begin + baby steps
+//                      (nearly constant count per d), then the k = 2 giant step
+//                      (always NUDUPL, Alg. 4 l.745) for all 32 lanes at once;
+//                      unfinished d go to the giant queue with their store.
+//   bsgs_giant_kernel  persistent lanes with per-lane refill from the queue
+//                      (giant counts are heavy-tailed).
 //
 // Per-lane state machine (the same functions run in the CPU emulation harness
 // tests/emu/kernel_emu.cu):
@@ -17,10 +26,11 @@
 //   HALF        fallback if the giant-step cap is hit: the half walk.
 //
 // Store ("dictionary of ideals", l.549, l.607): an open-addressing hash table of
-// u64 entries per lane in global memory (Q | P<<20 | t<<40 | log2-dist*256 <<42)
-// whose occupancy bits live in shared memory (so empty slots are never read
-// and never need clearing in HBM).  The paper's Bloom filter plays the same
-// role (no false negatives; positives verified exactly).
+// u64 entries per d in global memory, entry = Q | P<<20 | t<<40 | (2 log2 dist)<<51
+// (t unreduced, < 2^11); the occupancy bits live in shared memory while the
+// baby kernel fills the store and are then copied next to it, so empty slots
+// are never read and never cleared in HBM.  The paper's Bloom filter plays the
+// same role (no false negatives; positives verified exactly).
 #pragma once
 #include "common.cuh"
 #include "forms.cuh"
@@ -32,35 +42,18 @@ constexpr float GUARD_LOG2 = 1.0f / LN2F;    // "log mu'_k - log theta >= 1" in 
 enum LanePhase : u32 { PH_IDLE = 0, PH_BABY = 1, PH_GIANT = 2, PH_HALF = 3, PH_DONE = 4 };
 
 struct BsgsArgs {
-    u64 *tables;        // [lanes][ns] entries
-    int ns_log2;        // table slots per lane = 1 << ns_log2
+    int ns_log2;        // store slots per d = 1 << ns_log2
     int cap;            // max stored baby entries (load <= 1/2)
     float alpha;        // baby window factor: W = alpha d^(1/4)
     int plain_th;       // Alg. 4 plain-product threshold on Q (paper: 50)
     float giant_cap_mul;// giant-step cap = giant_cap_mul * (d^(1/4) + 10)
 };
 
-struct BsgsLane {
-    u64 d;
-    i64 L;              // floor(d^(1/4)) for NUCOMP's partial Euclid bound
-    double sqrtd;
-    float sqrtd_f, W2;  // W in log2 units
-    BabyState st;
-    float dist;         // log2 theta_{j+1} of the current baby ideal
-    int n_ent, extras;
-    u32 Q1, P1, t1;     // mu_1
-    float dist1;
-    u32 Qc, Pc, tc;     // mu'_{k-1}
-    float distc;
-    int k, kcap;
-    u32 phase, res;
-};
-
 // ---------------------------------------------------------------- the store --
 struct Store {
-    u32 *bm;            // occupancy bits: word w of this lane at bm[w * stride]
+    u32 *bm;            // occupancy bits: word w at bm[w * stride]
     int stride;
-    u64 *tab;           // this lane's slots
+    u64 *tab;           // slots of this d
     int ns_log2;
 };
 
@@ -72,12 +65,12 @@ EIS_HD void store_clear(Store &S) {
     for (int w = 0; w < (1 << S.ns_log2) / 32; w++) S.bm[w * S.stride] = 0;
 }
 
-EIS_HD void store_insert(Store &S, u32 Q, u32 P, u32 t, float dist2) {
+EIS_HD void store_insert(Store &S, u32 Q, u32 P, u32 traw, float dist2) {
     const u32 mask = (1u << S.ns_log2) - 1;
     u32 h = store_hash(Q, P, S.ns_log2);
-    float fx = dist2 * 256.0f + 0.5f;
-    u64 dfx = fx <= 0.f ? 0 : (fx >= 4194303.f ? 4194303ull : (u64)fx);
-    const u64 e = (u64)Q | ((u64)P << 20) | ((u64)t << 40) | (dfx << 42);
+    const float fx = dist2 * 2.0f;
+    const u64 dfx = fx <= 0.f ? 0 : (fx >= 8191.f ? 8191ull : (u64)fx);   // floor, 0.5 units
+    const u64 e = (u64)Q | ((u64)P << 20) | ((u64)(traw & 2047u) << 40) | (dfx << 51);
     for (;;) {
         u32 *wp = &S.bm[(h >> 5) * S.stride];
         const u32 w = *wp;
@@ -106,7 +99,20 @@ EIS_HD u64 store_lookup(const Store &S, u32 Q, u32 P) {
     }
 }
 
+EIS_HD u32 mod3(u32 v) { return v % 3u; }
+
 // ------------------------------------------------------------ baby phase --
+struct BsgsLane {
+    u64 d;
+    float sqrtd_f, W2;  // W in log2 units
+    BabyState st;
+    float dist;         // log2 theta_{j+1} of the current baby ideal
+    int n_ent, extras;
+    u32 Q1, P1, t1;     // mu_1 (t reduced mod 3)
+    float dist1;
+    u32 phase, res;
+};
+
 // rho step with the log2 of the generator multiplier (P_j + sqrt d)/Q_{j-1}
 EIS_HD bool rho_step_dist(BabyState &st, float sqrtd_f, float &dist) {
     const u32 num = st.P + st.s;
@@ -127,19 +133,13 @@ EIS_HD bool rho_step_dist(BabyState &st, float sqrtd_f, float &dist) {
     return (Qn == st.Qp) | eP;
 }
 
-EIS_HD u32 mod3(u32 v) { return v % 3u; }
-
 // Start d: store theta_1 and theta_2.  Returns true if d is already finished.
 EIS_HD bool bsgs_begin(BsgsLane &ln, Store &S, const BsgsArgs &B, u64 d) {
     ln.d = d;
     u32 r1;
     const bool fin = baby_init(ln.st, d, &r1);
-    ln.sqrtd = sqrt((double)d);
-    ln.sqrtd_f = (float)ln.sqrtd;
-    ln.L = (i64)isqrt_u64_dev((u64)ln.st.s);        // floor(d^(1/4))
-    const float d14 = sqrtf(ln.sqrtd_f);
-    ln.W2 = B.alpha * d14 / LN2F;
-    ln.kcap = (int)(B.giant_cap_mul * (d14 + 10.f));
+    ln.sqrtd_f = (float)sqrt((double)d);
+    ln.W2 = B.alpha * sqrtf(ln.sqrtd_f) / LN2F;
     if (fin) {
         ln.res = r1;
         ln.phase = PH_DONE;
@@ -150,7 +150,7 @@ EIS_HD bool bsgs_begin(BsgsLane &ln, Store &S, const BsgsArgs &B, u64 d) {
     store_insert(S, 2u, ln.st.P, 0u, 0.f);
     // theta_2 = ((P_1 + sqrt d)/2) theta_1 <-> (Q_1, P_1)
     ln.dist = log2_approx(((float)ln.st.P + ln.sqrtd_f) * 0.5f);
-    store_insert(S, ln.st.Q, ln.st.P, mod3(ln.st.t2 >> 1), ln.dist);
+    store_insert(S, ln.st.Q, ln.st.P, ln.st.t2 >> 1, ln.dist);
     ln.n_ent = 2;
     ln.extras = -1;
     ln.phase = PH_BABY;
@@ -170,16 +170,11 @@ EIS_HD int bsgs_baby(BsgsLane &ln, Store &S, const BsgsArgs &B, int kmax) {
             ln.extras = 2;                   // "Compute two more ideals" (l.560)
         }
         if (ln.extras == 0) {
-            ln.Qc = ln.Q1;
-            ln.Pc = ln.P1;
-            ln.tc = ln.t1;
-            ln.distc = ln.dist1;
-            ln.k = 1;
             ln.phase = PH_GIANT;
             return k;
         }
         const bool ex = rho_step_dist(ln.st, ln.sqrtd_f, ln.dist);
-        store_insert(S, ln.st.Q, ln.st.P, mod3(ln.st.t2 >> 1), ln.dist);
+        store_insert(S, ln.st.Q, ln.st.P, ln.st.t2 >> 1, ln.dist);
         ln.n_ent++;
         if (ex) {
             ln.res = baby_result(ln.st);
@@ -191,6 +186,39 @@ EIS_HD int bsgs_baby(BsgsLane &ln, Store &S, const BsgsArgs &B, int kmax) {
     return k;
 }
 
+// ----------------------------------------------------------- giant phase --
+struct GiantLane {
+    u64 d;
+    i64 s, L;           // isqrt(d), floor(d^(1/4))
+    double sqrtd;
+    Mu1Form m1;
+    u32 t1;
+    float dist1;
+    u32 Qc, Pc, tc;     // mu'_{k-1}
+    float distc;
+    int k, kcap;
+    u32 phase, res;
+};
+
+// Giant-phase state from mu_1 (k = 1: mu'_1 = mu_1).
+EIS_HD void giant_init(GiantLane &g, const BsgsArgs &B, u64 d, u32 Q1, u32 P1, u32 t1,
+                       float dist1, u32 *err) {
+    g.d = d;
+    g.s = (i64)isqrt_u64_dev(d);
+    g.L = (i64)isqrt_u64_dev((u64)g.s);            // floor(d^(1/4))
+    g.sqrtd = sqrt((double)d);
+    g.m1 = mu1_form((i64)Q1, (i64)P1, (i64)d, err);
+    g.t1 = t1;
+    g.dist1 = dist1;
+    g.Qc = Q1;
+    g.Pc = P1;
+    g.tc = t1;
+    g.distc = dist1;
+    g.k = 1;
+    g.kcap = (int)(B.giant_cap_mul * (sqrtf((float)g.s) + 10.f));
+    g.phase = PH_GIANT;
+}
+
 struct GiantInfo {
     u32 kind;       // composition kind
     u32 nred;       // rho steps in the reduction
@@ -198,15 +226,14 @@ struct GiantInfo {
 
 // One giant step.  Sets PH_DONE on a guarded hit, PH_HALF
 // when the cap is exceeded.  *err counts invariant violations.
-EIS_HD GiantInfo bsgs_giant(BsgsLane &ln, const Store &S, const BsgsArgs &B, u32 *err) {
+EIS_HD GiantInfo bsgs_giant(GiantLane &g, const Store &S, const BsgsArgs &B, u32 *err) {
     GiantInfo gi;
-    const i64 d = (i64)ln.d;
-    const i64 s = (i64)ln.st.s;
-    const Composed c = nucomp_choose((i64)ln.Q1, (i64)ln.P1, (i64)ln.Qc, (i64)ln.Pc, d, ln.L,
-                                     ln.sqrtd, B.plain_th, err);
+    const i64 d = (i64)g.d;
+    const i64 s = g.s;
+    const Composed c = nucomp_choose(g.m1, (i64)g.Qc, (i64)g.Pc, d, g.L, g.sqrtd, B.plain_th, err);
     gi.kind = c.kind;
-    u32 t = mod3(ln.t1 + ln.tc + 3u - c.tg);       // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
-    float dist = ln.dist1 + ln.distc - c.lg;
+    u32 t = mod3(g.t1 + g.tc + 3u - c.tg);       // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
+    float dist = g.dist1 + g.distc - c.lg;
     i64 Q = c.Q, P = c.P;
     u32 nred = 0;
     for (;;) {
@@ -216,126 +243,60 @@ EIS_HD GiantInfo bsgs_giant(BsgsLane &ln, const Store &S, const BsgsArgs &B, u32
         const i64 Pn = q * Q - P;
         const i64 Qn = exact_div(d - Pn * Pn, Q, err);
         t = mod3(t + 1u + (u32)((Pn >> 1) & 1));
-        dist += log2_approx((float)fabs((double)Pn + ln.sqrtd)) - log2_approx((float)Q);
+        dist += log2_approx((float)fabs((double)Pn + g.sqrtd)) - log2_approx((float)Q);
         P = Pn;
         Q = iabs64(Qn);
         if (++nred > 4096) { *err += 1; break; }
     }
     gi.nred = nred;
-    ln.k++;
+    g.k++;
     const u64 e = store_lookup(S, (u32)Q, (u32)P);
     if (e) {
-        const float de = (float)(e >> 42) * (1.0f / 256.0f);
+        const float de = (float)(e >> 51) * 0.5f;
         if (dist - de >= GUARD_LOG2) {
-            const u32 te = (u32)((e >> 40) & 3);
-            ln.res = mod3(t + 3u - te);             // eps = mu'_k / theta
-            ln.phase = PH_DONE;
+            const u32 te = mod3((u32)((e >> 40) & 2047u));
+            g.res = mod3(t + 3u - te);              // eps = mu'_k / theta
+            g.phase = PH_DONE;
             return gi;
         }
     }
-    ln.Qc = (u32)Q;
-    ln.Pc = (u32)P;
-    ln.tc = t;
-    ln.distc = dist;
-    if (ln.k > ln.kcap) ln.phase = PH_HALF;
+    g.Qc = (u32)Q;
+    g.Pc = (u32)P;
+    g.tc = t;
+    g.distc = dist;
+    if (g.k > g.kcap) g.phase = PH_HALF;
     return gi;
 }
 
-// --------------------------------------------------------------- the kernel --
+// ------------------------------------------------------------------ kernels --
+// per-d record handed from the baby kernel to the giant kernel (one sector)
+struct __align__(32) GiantRec {
+    u32 off, Q1, P1, Qc, Pc, tk;   // tk = t1 | tc << 2 | k << 4
+    float dist1, distc;
+};
+
+struct BsgsOut {
+    u64 *tables;        // [segment survivors][ns] store slots
+    u32 *bms;           // [segment survivors][ns/32] occupancy words
+    GiantRec *recs;     // [segment survivors]
+    u32 *queue;         // survivor indices needing giant steps
+    u32 *qcount;        // device: queue length
+    u32 *qwork;         // device: giant-kernel work counter
+};
+
 #ifdef __CUDACC__
-template <int KB>
-__global__ void __launch_bounds__(256)
-walk_bsgs_kernel(WalkArgs a, BsgsArgs B) {
-    extern __shared__ u32 smem[];
-    u32 *hist = smem;                              // 2 * HIST_CAP
-    u32 *bmap = smem + 2 * HIST_CAP;               // (ns/32) words x blockDim
-    for (int i = threadIdx.x; i < 2 * a.nb; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-
-    const int lane = threadIdx.x & 31;
-    const u32 n = *a.count;
-    const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    Store S;
-    S.bm = bmap + threadIdx.x;
-    S.stride = blockDim.x;
-    S.tab = B.tables + (gtid << B.ns_log2);
-    S.ns_log2 = B.ns_log2;
-
-    BsgsLane ln;
-    ln.phase = PH_IDLE;
-    u32 off = 0;
-    bool exhausted = false;
-    u32 n_done = 0, n_sym = 0, n_fb = 0;
-    u64 baby = 0, giant = 0, red = 0;
-    u32 err = 0;
-
-    auto finish = [&]() {
-        const u32 t = ln.res % 3;
-        n_done++;
-        if (a.flags) a.flags[off] = (u8)t;
-        if (a.ckpt) {
-            const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, ln.d) - a.b_lo;
-            atomicAdd(&hist[b], 1u);
-            if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
-        }
-        ln.phase = PH_IDLE;
-    };
-
-    for (;;) {
-        const u32 need = __ballot_sync(FULL_MASK, ln.phase == PH_IDLE && !exhausted);
-        if (need) {
-            const int leader = __ffs(need) - 1;
-            u32 base = 0;
-            if (lane == leader) base = atomicAdd(a.work, (u32)__popc(need));
-            base = __shfl_sync(FULL_MASK, base, leader);
-            if (ln.phase == PH_IDLE && !exhausted) {
-                const u32 idx = base + __popc(need & lanemask_lt());
-                if (idx < n) {
-                    off = __ldg(a.list + idx);
-                    baby += 1;
-                    if (bsgs_begin(ln, S, B, cand_d(a.i0 + off))) { n_sym++; finish(); }
-                } else {
-                    exhausted = true;
-                }
-            }
-        }
-        if (__all_sync(FULL_MASK, exhausted && ln.phase == PH_IDLE)) break;
-        if (ln.phase == PH_BABY) {
-            baby += bsgs_baby(ln, S, B, KB);
-            if (ln.phase == PH_DONE) n_sym++;
-        }
-        if (ln.phase == PH_GIANT) {
-            const GiantInfo gi = bsgs_giant(ln, S, B, &err);
-            giant++;
-            red += gi.nred;
-            if (ln.phase == PH_HALF) {
-                n_fb++;
-                u32 r1;
-                if (baby_init(ln.st, ln.d, &r1)) { ln.res = r1; ln.phase = PH_DONE; }
-            }
-        }
-        if (ln.phase == PH_HALF) {
-            for (int k = 0; k < KB; k++) {
-                baby++;
-                if (baby_step(ln.st)) { ln.res = baby_result(ln.st); ln.phase = PH_DONE; break; }
-            }
-        }
-        if (ln.phase == PH_DONE) finish();
+__device__ __forceinline__ void record_result(const WalkArgs &a, u32 *hist, u32 off, u64 d,
+                                              u32 res) {
+    const u32 t = res % 3;
+    if (a.flags) a.flags[off] = (u8)t;
+    if (a.ckpt) {
+        const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
+        atomicAdd(&hist[b], 1u);
+        if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
     }
+}
 
-    const u64 s_baby = warp_sum_u64(baby), s_giant = warp_sum_u64(giant),
-              s_red = warp_sum_u64(red), s_done = warp_sum_u64(n_done),
-              s_sym = warp_sum_u64(n_sym), s_fb = warp_sum_u64(n_fb);
-    const u32 s_err = __reduce_add_sync(FULL_MASK, err);
-    if (lane == 0 && a.stats) {
-        atomicAdd((unsigned long long *)&a.stats[ST_BABY], (unsigned long long)s_baby);
-        atomicAdd((unsigned long long *)&a.stats[ST_GIANT], (unsigned long long)s_giant);
-        atomicAdd((unsigned long long *)&a.stats[ST_REDUCE], (unsigned long long)s_red);
-        atomicAdd((unsigned long long *)&a.stats[ST_D], (unsigned long long)s_done);
-        atomicAdd((unsigned long long *)&a.stats[ST_SYM], (unsigned long long)s_sym);
-        atomicAdd((unsigned long long *)&a.stats[ST_FALLBACK], (unsigned long long)s_fb);
-    }
-    if (lane == 0 && s_err) atomicAdd(a.err, s_err);
+__device__ __forceinline__ void flush_hist(const WalkArgs &a, u32 *hist) {
     __syncthreads();
     if (a.ckpt) {
         for (int i = threadIdx.x; i < a.nb; i += blockDim.x) {
@@ -348,57 +309,276 @@ walk_bsgs_kernel(WalkArgs a, BsgsArgs B) {
     }
 }
 
+__device__ __forceinline__ void flush_stats(const WalkArgs &a, u64 baby, u64 giant, u64 red,
+                                            u64 done, u64 sym, u64 fb, u32 err) {
+    const int lane = threadIdx.x & 31;
+    const u64 s_baby = warp_sum_u64(baby), s_giant = warp_sum_u64(giant),
+              s_red = warp_sum_u64(red), s_done = warp_sum_u64(done), s_sym = warp_sum_u64(sym),
+              s_fb = warp_sum_u64(fb);
+    const u32 s_err = __reduce_add_sync(FULL_MASK, err);
+    if (lane == 0 && a.stats) {
+        atomicAdd((unsigned long long *)&a.stats[ST_BABY], (unsigned long long)s_baby);
+        atomicAdd((unsigned long long *)&a.stats[ST_GIANT], (unsigned long long)s_giant);
+        atomicAdd((unsigned long long *)&a.stats[ST_REDUCE], (unsigned long long)s_red);
+        atomicAdd((unsigned long long *)&a.stats[ST_D], (unsigned long long)s_done);
+        atomicAdd((unsigned long long *)&a.stats[ST_SYM], (unsigned long long)s_sym);
+        atomicAdd((unsigned long long *)&a.stats[ST_FALLBACK], (unsigned long long)s_fb);
+    }
+    if (lane == 0 && s_err) atomicAdd(a.err, s_err);
+}
+
+template <int KB>
+__global__ void __launch_bounds__(256)
+bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
+    extern __shared__ u32 smem[];
+    u32 *hist = smem;                              // 2 * HIST_CAP
+    u32 *bmap = smem + 2 * HIST_CAP;               // (ns/32) words x blockDim
+    for (int i = threadIdx.x; i < 2 * a.nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const u32 n = *a.count;
+    const int nw = (1 << B.ns_log2) / 32;
+    Store S;
+    S.bm = bmap + threadIdx.x;
+    S.stride = blockDim.x;
+    S.ns_log2 = B.ns_log2;
+    u64 baby = 0, giant = 0, red = 0, done = 0, sym = 0;
+    u32 err = 0;
+
+    for (;;) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(a.work, 32u);
+        base = __shfl_sync(FULL_MASK, base, 0);
+        if (base >= n) break;
+        const u32 idx = base + lane;
+        BsgsLane ln;
+        ln.phase = PH_IDLE;
+        u32 off = 0;
+        if (idx < n) {
+            off = __ldg(a.list + idx);
+            S.tab = o.tables + ((u64)idx << B.ns_log2);
+            baby += 1;
+            if (bsgs_begin(ln, S, B, cand_d(a.i0 + off))) {
+                record_result(a, hist, off, ln.d, ln.res);
+                done++;
+                sym++;
+                ln.phase = PH_IDLE;
+            }
+        }
+        while (__any_sync(FULL_MASK, ln.phase == PH_BABY)) {
+            if (ln.phase == PH_BABY) {
+                baby += bsgs_baby(ln, S, B, KB);
+                if (ln.phase == PH_DONE) {
+                    record_result(a, hist, off, ln.d, ln.res);
+                    done++;
+                    sym++;
+                    ln.phase = PH_IDLE;
+                }
+            }
+        }
+        // k = 2 for all lanes together: mu_2 = mu_1 * mu_1 (NUDUPL)
+        bool push = false;
+        if (ln.phase == PH_GIANT) {
+            GiantLane g;
+            giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
+            const GiantInfo gi = bsgs_giant(g, S, B, &err);
+            giant++;
+            red += gi.nred;
+            if (g.phase == PH_DONE) {
+                record_result(a, hist, off, ln.d, g.res);
+                done++;
+            } else {
+                GiantRec r;
+                r.off = off;
+                r.Q1 = ln.Q1;
+                r.P1 = ln.P1;
+                r.Qc = g.Qc;
+                r.Pc = g.Pc;
+                r.tk = g.t1 | (g.tc << 2) | ((u32)g.k << 4);
+                r.dist1 = g.dist1;
+                r.distc = g.distc;
+                o.recs[idx] = r;
+                u32 *dst = o.bms + (u64)idx * nw;
+                for (int w = 0; w < nw; w++) dst[w] = S.bm[w * S.stride];
+                push = true;
+            }
+        }
+        const u32 pm = __ballot_sync(FULL_MASK, push);
+        if (pm) {
+            u32 qb = 0;
+            const int leader = __ffs(pm) - 1;
+            if (lane == leader) qb = atomicAdd(o.qcount, (u32)__popc(pm));
+            qb = __shfl_sync(FULL_MASK, qb, leader);
+            if (push) o.queue[qb + __popc(pm & lanemask_lt())] = idx;
+        }
+    }
+    flush_stats(a, baby, giant, red, done, sym, 0, err);
+    flush_hist(a, hist);
+}
+
+__global__ void __launch_bounds__(256)
+bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
+    __shared__ u32 hist[2 * HIST_CAP];
+    for (int i = threadIdx.x; i < 2 * a.nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const u32 nq = *o.qcount;
+    const int nw = (1 << B.ns_log2) / 32;
+    Store S;
+    S.stride = 1;
+    S.ns_log2 = B.ns_log2;
+    S.bm = nullptr;
+    S.tab = nullptr;
+    GiantLane g;
+    g.phase = PH_IDLE;
+    u32 off = 0;
+    bool exhausted = false;
+    u64 baby = 0, giant = 0, red = 0, done = 0, fb = 0;
+    u32 err = 0;
+
+    for (;;) {
+        const u32 need = __ballot_sync(FULL_MASK, g.phase == PH_IDLE && !exhausted);
+        if (need) {
+            const int leader = __ffs(need) - 1;
+            u32 base = 0;
+            if (lane == leader) base = atomicAdd(o.qwork, (u32)__popc(need));
+            base = __shfl_sync(FULL_MASK, base, leader);
+            if (g.phase == PH_IDLE && !exhausted) {
+                const u32 qi = base + __popc(need & lanemask_lt());
+                if (qi < nq) {
+                    const u32 idx = __ldg(o.queue + qi);
+                    const GiantRec r = o.recs[idx];
+                    off = r.off;
+                    giant_init(g, B, cand_d(a.i0 + off), r.Q1, r.P1, r.tk & 3u, r.dist1, &err);
+                    g.Qc = r.Qc;
+                    g.Pc = r.Pc;
+                    g.tc = (r.tk >> 2) & 3u;
+                    g.k = (int)(r.tk >> 4);
+                    g.distc = r.distc;
+                    S.bm = o.bms + (u64)idx * nw;
+                    S.tab = o.tables + ((u64)idx << B.ns_log2);
+                } else {
+                    exhausted = true;
+                }
+            }
+        }
+        if (__all_sync(FULL_MASK, exhausted && g.phase == PH_IDLE)) break;
+        if (g.phase == PH_GIANT) {
+            const GiantInfo gi = bsgs_giant(g, S, B, &err);
+            giant++;
+            red += gi.nred;
+            if (g.phase == PH_HALF) {     // cap exceeded: exact half walk instead
+                fb++;
+                BabyState st;
+                u32 r1;
+                if (baby_init(st, g.d, &r1)) {
+                    g.res = r1;
+                } else {
+                    do { baby++; } while (!baby_step(st));
+                    g.res = baby_result(st);
+                }
+                g.phase = PH_DONE;
+            }
+        }
+        if (g.phase == PH_DONE) {
+            record_result(a, hist, off, g.d, g.res);
+            done++;
+            g.phase = PH_IDLE;
+        }
+    }
+    flush_stats(a, baby, giant, red, done, 0, fb, err);
+    flush_hist(a, hist);
+}
+
 // ------------------------------------------------------------- host launch --
 struct BsgsScratch {
     u64 *tables = nullptr;
-    size_t bytes = 0;
+    size_t tables_bytes = 0;
+    u32 *bms = nullptr;
+    size_t bms_bytes = 0;
+    GiantRec *recs = nullptr;
+    size_t recs_n = 0;
+    u32 *queue = nullptr;
+    size_t queue_n = 0;
 };
 
 inline void bsgs_free(BsgsScratch &s) {
     if (s.tables) cudaFree(s.tables);
-    s.tables = nullptr;
-    s.bytes = 0;
+    if (s.bms) cudaFree(s.bms);
+    if (s.recs) cudaFree(s.recs);
+    if (s.queue) cudaFree(s.queue);
+    s = BsgsScratch();
 }
 
 constexpr int BSGS_KB = 8;
 constexpr int BSGS_THREADS = 256;
 
-// table size for a segment whose largest d is d_max
+// store size for a segment whose largest d is d_max (load <= 1/2)
 inline int bsgs_ns_log2(u64 d_max, float alpha) {
-    const double w = alpha * std::pow((double)d_max, 0.25);   // nats
-    const double need = 2.0 * (w / 0.9 + 8.0);
+    const double w = alpha * std::pow((double)d_max, 0.25);   // window in nats
+    const double need = 2.0 * (w / 1.1 + 8.0);                // ~1.2 nats per baby step
     int l = 6;
     while ((double)(1 << l) < need && l < 10) l++;
     return l;
 }
 
-inline int launch_bsgs(const WalkArgs &a, u64 d_lo, u64 d_hi, int num_sms, int alpha_x16,
-                       BsgsScratch &scr, u32 *, cudaStream_t s, int *launches) {
-    (void)d_lo;
+template <class T>
+inline int bsgs_grow(T *&p, size_t &cap, size_t n) {
+    if (n <= cap && p) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return -3;
+    cap = n;
+    return 0;
+}
+
+// max survivors of a segment of `len` candidates (upper bound: all of them)
+inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
+                       BsgsScratch &scr, u32 *qctr, cudaStream_t s, int *launches) {
     BsgsArgs B;
     B.alpha = alpha_x16 / 16.0f;
     B.ns_log2 = bsgs_ns_log2(d_hi, B.alpha);
     B.cap = (1 << B.ns_log2) / 2 - 2;
     B.plain_th = 50;
     B.giant_cap_mul = 20.0f;
+    const size_t n = (size_t)seg_len;
+    size_t tb = scr.tables_bytes, bb = scr.bms_bytes;
+    if (bsgs_grow(scr.tables, tb, n << B.ns_log2)) return -3;
+    scr.tables_bytes = tb;
+    if (bsgs_grow(scr.bms, bb, n * ((1 << B.ns_log2) / 32))) return -3;
+    scr.bms_bytes = bb;
+    if (bsgs_grow(scr.recs, scr.recs_n, n)) return -3;
+    if (bsgs_grow(scr.queue, scr.queue_n, n)) return -3;
+    BsgsOut o;
+    o.tables = scr.tables;
+    o.bms = scr.bms;
+    o.recs = scr.recs;
+    o.queue = scr.queue;
+    o.qcount = qctr;
+    o.qwork = qctr + 1;
+    if (cudaMemsetAsync(qctr, 0, 2 * sizeof(u32), s) != cudaSuccess) return -4;
+
     const size_t smem = (size_t)(2 * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * BSGS_THREADS * 4;
-    if (cudaFuncSetAttribute(walk_bsgs_kernel<BSGS_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(bsgs_baby_kernel<BSGS_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return -4;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_bsgs_kernel<BSGS_KB>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_baby_kernel<BSGS_KB>,
                                                       BSGS_THREADS, smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
-    const unsigned blocks = (unsigned)(num_sms * per_sm);
-    const size_t need = (size_t)blocks * BSGS_THREADS * ((size_t)1 << B.ns_log2) * sizeof(u64);
-    if (need > scr.bytes) {
-        bsgs_free(scr);
-        if (cudaMalloc(&scr.tables, need) != cudaSuccess) return -3;
-        scr.bytes = need;
-    }
-    B.tables = scr.tables;
-    walk_bsgs_kernel<BSGS_KB><<<blocks, BSGS_THREADS, smem, s>>>(a, B);
+    bsgs_baby_kernel<BSGS_KB><<<(unsigned)(num_sms * per_sm), BSGS_THREADS, smem, s>>>(a, B, o);
+    (*launches)++;
+    if (cudaGetLastError() != cudaSuccess) return -4;
+    int per_sm_g = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_g, bsgs_giant_kernel, BSGS_THREADS,
+                                                      0) != cudaSuccess ||
+        per_sm_g < 1)
+        return -4;
+    bsgs_giant_kernel<<<(unsigned)(num_sms * per_sm_g), BSGS_THREADS, 0, s>>>(a, B, o);
     (*launches)++;
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }

@@ -49,25 +49,30 @@ int main(int argc, char **argv) {
             BsgsLane ln;
             baby = 1;
             bsgs_begin(ln, S, B, d);
-            while (ln.phase != PH_DONE) {
-                if (ln.phase == PH_BABY) baby += bsgs_baby(ln, S, B, 8);
-                if (ln.phase == PH_GIANT) {
-                    GiantInfo gi = bsgs_giant(ln, S, B, &err);
+            while (ln.phase == PH_BABY) baby += bsgs_baby(ln, S, B, 8);
+            if (ln.phase == PH_DONE) {
+                res = ln.res;
+            } else {
+                GiantLane g;
+                giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
+                while (g.phase == PH_GIANT) {
+                    GiantInfo gi = bsgs_giant(g, S, B, &err);
                     giant++;
                     red += gi.nred;
                     kinds[gi.kind]++;
-                    if (ln.phase == PH_HALF) {
-                        fb++;
-                        u32 r1;
-                        if (baby_init(ln.st, ln.d, &r1)) { ln.res = r1; ln.phase = PH_DONE; }
+                }
+                if (g.phase == PH_HALF) {
+                    fb++;
+                    BabyState st;
+                    u32 r1;
+                    if (baby_init(st, ln.d, &r1)) g.res = r1;
+                    else {
+                        do { baby++; } while (!baby_step(st));
+                        g.res = baby_result(st);
                     }
                 }
-                if (ln.phase == PH_HALF) {
-                    baby++;
-                    if (baby_step(ln.st)) { ln.res = baby_result(ln.st); ln.phase = PH_DONE; }
-                }
+                res = g.res;
             }
-            res = ln.res;
         }
         printf("%llu %u %llu %llu %llu %llu %u %llu %llu %llu\n", d, res % 3,
                (unsigned long long)baby, (unsigned long long)giant, (unsigned long long)red,
