@@ -27,10 +27,13 @@
 //
 // Store ("dictionary of ideals", l.549, l.607): an open-addressing hash table of
 // u64 entries per d in global memory, entry = Q | P<<20 | t<<40 | (2 log2 dist)<<51
-// (t unreduced, < 2^11); the occupancy bits live in shared memory while the
-// baby kernel fills the store and are then copied next to it, so empty slots
-// are never read and never cleared in HBM.  The paper's Bloom filter plays the
-// same role (no false negatives; positives verified exactly).
+// (t unreduced, < 2^11).  The baby kernel zero-fills the 32 stores of a warp
+// batch with coalesced 16-byte stores (they are contiguous), so the scattered
+// 8-byte slot writes that follow land in complete, L2-resident sectors (no DRAM
+// read-modify-write); free slots are found through occupancy bits in shared
+// memory (no global reads while inserting), and lookups stop at a zero slot.
+// The paper's Bloom filter plays the same role (no false negatives; positives
+// verified exactly).
 #pragma once
 #include "common.cuh"
 #include "forms.cuh"
@@ -85,16 +88,15 @@ EIS_HD void store_insert(Store &S, u32 Q, u32 P, u32 traw, float dist2) {
     }
 }
 
-// returns the entry or 0
-EIS_HD u64 store_lookup(const Store &S, u32 Q, u32 P) {
-    const u32 mask = (1u << S.ns_log2) - 1;
+// returns the entry or 0.  Stores are zero-filled before use (an entry is never
+// 0: Q >= 2), so probing stops at the first empty slot without the bitmap.
+EIS_HD u64 store_lookup(const u64 *tab, int ns_log2, u32 Q, u32 P) {
+    const u32 mask = (1u << ns_log2) - 1;
     const u64 key = (u64)Q | ((u64)P << 20);
-    u32 h = store_hash(Q, P, S.ns_log2);
+    u32 h = store_hash(Q, P, ns_log2);
     for (;;) {
-        const u32 w = S.bm[(h >> 5) * S.stride];
-        if (!((w >> (h & 31)) & 1)) return 0;
-        const u64 e = S.tab[h];
-        if ((e & 0xFFFFFFFFFFull) == key) return e;
+        const u64 e = tab[h];
+        if (e == 0 || (e & 0xFFFFFFFFFFull) == key) return e;
         h = (h + 1) & mask;
     }
 }
@@ -226,7 +228,7 @@ struct GiantInfo {
 
 // One giant step.  Sets PH_DONE on a guarded hit, PH_HALF
 // when the cap is exceeded.  *err counts invariant violations.
-EIS_HD GiantInfo bsgs_giant(GiantLane &g, const Store &S, const BsgsArgs &B, u32 *err) {
+EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u64 *tab, const BsgsArgs &B, u32 *err) {
     GiantInfo gi;
     const i64 d = (i64)g.d;
     const i64 s = g.s;
@@ -250,7 +252,7 @@ EIS_HD GiantInfo bsgs_giant(GiantLane &g, const Store &S, const BsgsArgs &B, u32
     }
     gi.nred = nred;
     g.k++;
-    const u64 e = store_lookup(S, (u32)Q, (u32)P);
+    const u64 e = store_lookup(tab, B.ns_log2, (u32)Q, (u32)P);
     if (e) {
         const float de = (float)(e >> 51) * 0.5f;
         if (dist - de >= GUARD_LOG2) {
@@ -277,7 +279,6 @@ struct __align__(32) GiantRec {
 
 struct BsgsOut {
     u64 *tables;        // [segment survivors][ns] store slots
-    u32 *bms;           // [segment survivors][ns/32] occupancy words
     GiantRec *recs;     // [segment survivors]
     u32 *queue;         // survivor indices needing giant steps
     u32 *qcount;        // device: queue length
@@ -338,7 +339,6 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 
     const int lane = threadIdx.x & 31;
     const u32 n = *a.count;
-    const int nw = (1 << B.ns_log2) / 32;
     Store S;
     S.bm = bmap + threadIdx.x;
     S.stride = blockDim.x;
@@ -352,6 +352,13 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         base = __shfl_sync(FULL_MASK, base, 0);
         if (base >= n) break;
         const u32 idx = base + lane;
+        {   // zero the batch's 32 contiguous stores (coalesced, full lines)
+            uint4 *z = reinterpret_cast<uint4 *>(o.tables + ((u64)base << B.ns_log2));
+            const u32 nz = (min(n - base, 32u) << B.ns_log2) / 2;
+            const uint4 zero = make_uint4(0, 0, 0, 0);
+            for (u32 c = lane; c < nz; c += 32) z[c] = zero;
+            __syncwarp();
+        }
         BsgsLane ln;
         ln.phase = PH_IDLE;
         u32 off = 0;
@@ -382,7 +389,7 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         if (ln.phase == PH_GIANT) {
             GiantLane g;
             giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
-            const GiantInfo gi = bsgs_giant(g, S, B, &err);
+            const GiantInfo gi = bsgs_giant(g, S.tab, B, &err);
             giant++;
             red += gi.nred;
             if (g.phase == PH_DONE) {
@@ -399,8 +406,6 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 r.dist1 = g.dist1;
                 r.distc = g.distc;
                 o.recs[idx] = r;
-                u32 *dst = o.bms + (u64)idx * nw;
-                for (int w = 0; w < nw; w++) dst[w] = S.bm[w * S.stride];
                 push = true;
             }
         }
@@ -425,12 +430,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 
     const int lane = threadIdx.x & 31;
     const u32 nq = *o.qcount;
-    const int nw = (1 << B.ns_log2) / 32;
-    Store S;
-    S.stride = 1;
-    S.ns_log2 = B.ns_log2;
-    S.bm = nullptr;
-    S.tab = nullptr;
+    const u64 *tab = nullptr;
     GiantLane g;
     g.phase = PH_IDLE;
     u32 off = 0;
@@ -457,8 +457,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                     g.tc = (r.tk >> 2) & 3u;
                     g.k = (int)(r.tk >> 4);
                     g.distc = r.distc;
-                    S.bm = o.bms + (u64)idx * nw;
-                    S.tab = o.tables + ((u64)idx << B.ns_log2);
+                    tab = o.tables + ((u64)idx << B.ns_log2);
                 } else {
                     exhausted = true;
                 }
@@ -466,7 +465,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         if (__all_sync(FULL_MASK, exhausted && g.phase == PH_IDLE)) break;
         if (g.phase == PH_GIANT) {
-            const GiantInfo gi = bsgs_giant(g, S, B, &err);
+            const GiantInfo gi = bsgs_giant(g, tab, B, &err);
             giant++;
             red += gi.nred;
             if (g.phase == PH_HALF) {     // cap exceeded: exact half walk instead
@@ -496,8 +495,6 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 struct BsgsScratch {
     u64 *tables = nullptr;
     size_t tables_bytes = 0;
-    u32 *bms = nullptr;
-    size_t bms_bytes = 0;
     GiantRec *recs = nullptr;
     size_t recs_n = 0;
     u32 *queue = nullptr;
@@ -506,7 +503,6 @@ struct BsgsScratch {
 
 inline void bsgs_free(BsgsScratch &s) {
     if (s.tables) cudaFree(s.tables);
-    if (s.bms) cudaFree(s.bms);
     if (s.recs) cudaFree(s.recs);
     if (s.queue) cudaFree(s.queue);
     s = BsgsScratch();
@@ -545,16 +541,13 @@ inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, in
     B.plain_th = 50;
     B.giant_cap_mul = 20.0f;
     const size_t n = (size_t)seg_len;
-    size_t tb = scr.tables_bytes, bb = scr.bms_bytes;
-    if (bsgs_grow(scr.tables, tb, n << B.ns_log2)) return -3;
+    size_t tb = scr.tables_bytes;
+    if (bsgs_grow(scr.tables, tb, (n + 32) << B.ns_log2)) return -3;   // +32: batch tail
     scr.tables_bytes = tb;
-    if (bsgs_grow(scr.bms, bb, n * ((1 << B.ns_log2) / 32))) return -3;
-    scr.bms_bytes = bb;
     if (bsgs_grow(scr.recs, scr.recs_n, n)) return -3;
     if (bsgs_grow(scr.queue, scr.queue_n, n)) return -3;
     BsgsOut o;
     o.tables = scr.tables;
-    o.bms = scr.bms;
     o.recs = scr.recs;
     o.queue = scr.queue;
     o.qcount = qctr;

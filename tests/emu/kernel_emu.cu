@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <algorithm>
 
 #include "../../paper_2507_06579_b200/csrc/walk_bsgs.cuh"
 
@@ -46,6 +47,7 @@ int main(int argc, char **argv) {
             S.stride = 1;
             S.tab = tab.data();
             S.ns_log2 = B.ns_log2;
+            std::fill(tab.begin(), tab.begin() + (1 << B.ns_log2), 0ull);
             BsgsLane ln;
             baby = 1;
             bsgs_begin(ln, S, B, d);
@@ -56,7 +58,7 @@ int main(int argc, char **argv) {
                 GiantLane g;
                 giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
                 while (g.phase == PH_GIANT) {
-                    GiantInfo gi = bsgs_giant(g, S, B, &err);
+                    GiantInfo gi = bsgs_giant(g, S.tab, B, &err);
                     giant++;
                     red += gi.nred;
                     kinds[gi.kind]++;
