@@ -91,6 +91,35 @@ EIS_HD i64 xgcd_s(i64 a, i64 b, i64 &x, i64 &y) {
     return g;
 }
 
+// ---- Euclid in exact FP32 integer arithmetic.  Every value below is an
+// integer of magnitude < 2^24, so FFMA/FADD on them are exact; the quotient
+// round(a * rcp(b)) is floor(a/b) or floor(a/b)+1 (|a/b| < 2^20, relative rcp
+// error < 2^-22) and one compare fixes it.  No integer<->float conversion
+// inside the loops (the XU pipe is narrow).
+constexpr float FMAGIC = 8388608.0f;   // 2^23
+
+EIS_HD float ffloor_div_pos(float a, float b) {   // floor(a/b), 0 <= a, 0 < b, exact ints
+    float q = fmaf(a, rcp_approx(b), FMAGIC) - FMAGIC;
+    if (fmaf(-q, b, a) < 0.f) q -= 1.f;
+    return q;
+}
+
+// g = gcd(a, b) and x with x a = g (mod b), for 0 <= a, b < 2^24 (exact floats).
+EIS_HD float fxgcd_x(float a, float b, float &x) {
+    float x0 = 1.f, x1 = 0.f;
+    while (b != 0.f) {
+        const float q = ffloor_div_pos(a, b);
+        const float r = fmaf(-q, b, a);
+        a = b;
+        b = r;
+        const float t = fmaf(-q, x1, x0);
+        x0 = x1;
+        x1 = t;
+    }
+    x = x0;
+    return a;
+}
+
 // exact division of small integers: |a| < 2^23, 0 < b < 2^23, b | a
 EIS_HD i64 sdiv_exact23(i64 a, i64 b) {
     const u32 q = udiv23((u32)iabs64(a), (u32)b);
@@ -130,37 +159,39 @@ EIS_HD u32 t_gamma(i64 x, i64 y, i64 v3) {
 // log2|gamma|, gamma = G (a + y sqrt d)/(2 u3), a = 2 x u3 + y v3.  If a and y
 // have opposite signs the sum cancels; then use |N(gamma)| = (Q1/2)(Q2/2)/|u3|
 // (norms of the ideals, R29) and the conjugate, which does not cancel.
-EIS_HD float log2_gamma(i64 G, i64 x, i64 y, i64 u3, i64 v3, double sqrtd, i64 Q1, i64 Q2) {
+EIS_HD float log2_gamma(i64 G, i64 x, i64 y, i64 u3, i64 v3, float sqrtd_f, i64 Q1, i64 Q2) {
     const i64 a = 2 * x * u3 + y * v3;
-    const double mag = fabs((double)a) + fabs((double)y) * sqrtd;   // |a| + |y| sqrt d
-    const float lconj = log2_approx((float)G) + log2_approx((float)mag) -
-                        log2_approx((float)iabs64(2 * u3));
-    if ((a >= 0) == (y >= 0) || a == 0 || y == 0) return lconj;  // no cancellation
-    const float lnorm = log2_approx((float)(Q1 >> 1)) + log2_approx((float)(Q2 >> 1)) -
-                        log2_approx((float)iabs64(u3));
-    return lnorm - lconj;
+    const float mag = fabsf((float)a) + fabsf((float)y) * sqrtd_f;   // |a| + |y| sqrt d
+    const float au3 = fabsf((float)u3);
+    if ((a >= 0) == (y >= 0) || a == 0 || y == 0)                    // no cancellation
+        return log2_approx((float)G * mag / (2.f * au3));
+    // log|gamma| = log|N(gamma)| - log|conj gamma|, |N| = (Q1/2)(Q2/2)/|u3|
+    return log2_approx(2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1) / ((float)G * mag));
 }
 
-// Partial Euclid of Algs. 2-3.
+// Partial Euclid of Algs. 2-3, in exact FP32
+// (0 <= bx < by < 2^23 on entry: bx = Bx mod By, By = u1/G).
 EIS_HD void partial_euclid(i64 &bx, i64 &by, i64 &x, i64 &y, int &z, i64 L) {
-    // 0 <= bx < by < 2^23 on entry (bx = Bx mod By, By = u1/G)
-    i32 bx32 = (i32)bx, by32 = (i32)by, x32 = 1, y32 = 0;
+    float fbx = (float)bx, fby = (float)by, fx = 1.f, fy = 0.f;
+    const float fL = (float)L;
     z = 0;
-    while (by32 > L && bx32 != 0) {
-        const i32 q = (i32)udiv23((u32)by32, (u32)bx32);
-        i32 t = by32 - q * bx32;
-        by32 = bx32; bx32 = t;
-        t = y32 - q * x32;
-        y32 = x32; x32 = t;
+    while (fby > fL && fbx != 0.f) {
+        const float q = ffloor_div_pos(fby, fbx);
+        const float t = fmaf(-q, fbx, fby);
+        fby = fbx;
+        fbx = t;
+        const float u = fmaf(-q, fx, fy);
+        fy = fx;
+        fx = u;
         z++;
     }
-    if (z & 1) { by32 = -by32; y32 = -y32; }
-    bx = bx32; by = by32; x = x32; y = y32;
+    if (z & 1) { fby = -fby; fy = -fy; }
+    bx = (i64)fbx; by = (i64)fby; x = (i64)fx; y = (i64)fy;
 }
 
 // Algorithm 2 NUCOMP on forms (u1,v1,w1), (u2,v2,w2).
 EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u3, i64 &v3,
-                   i64 &w3, i64 &G, i64 &xo, i64 &yo, u32 *err) {
+                   i64 &G, i64 &xo, i64 &yo, u32 *err) {
     if (w1 < w2) {
         i64 t;
         t = u1; u1 = u2; u2 = t;
@@ -169,16 +200,21 @@ EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u
     }
     const i64 s = (v1 + v2) / 2;    // exact: v1, v2 odd
     const i64 m = v2 - s;
-    i64 b, c;
-    const i64 F = xgcd(u2, u1, b, c);   // b u2 + c u1 = F
+    float fb;
+    const i64 F = (i64)fxgcd_x((float)u2, (float)u1, fb);   // b u2 + c u1 = F
+    const i64 b = (i64)fb;
     i64 Bx, By, Cy, Dy;
-    if (divides23(F, s)) {
+    if (F == 1 || divides23(F, s)) {
         G = F;
         Bx = m * b;
-        By = sdiv_exact23(u1, G);
-        Cy = sdiv_exact23(u2, G);
-        Dy = sdiv_exact23(s, G);
+        if (F == 1) { By = u1; Cy = u2; Dy = s; }
+        else {
+            By = sdiv_exact23(u1, G);
+            Cy = sdiv_exact23(u2, G);
+            Dy = sdiv_exact23(s, G);
+        }
     } else {
+        const i64 c = exact_div(F - b * u2, u1, err);
         i64 xx, yy;
         G = xgcd_s(F, s, xx, yy);       // xx F + yy s = G
         const i64 H = sdiv_exact23(F, G);
@@ -192,7 +228,7 @@ EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u
     i64 bx = floor_mod(Bx, By), by = By, x, y;
     int z;
     partial_euclid(bx, by, x, y, z, L);
-    const i64 ax = G * x, ay = G * y;
+    const i64 ay = G * y;
     if (z != 0) {
         const double rBy = rcp64((double)By);
         const i64 cx = exact_div_r(Cy * bx - m * x, By, rBy, err);
@@ -206,24 +242,24 @@ EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u
         if (bx != 0) cy = exact_div(Q2, bx, err);
         else cy = exact_div(cx * dy - w1, dx, err);
         u3 = by * cy - ay * dy;
-        w3 = bx * cx - ax * dx;
-        v3 = G * (Q3 + Q4) - Q1 - Q2;
+        v3 = G * (Q3 + Q4) - Q1 - Q2;      // (w3 = bx cx - ax dx is not needed)
     } else {
         const double rBy = rcp64((double)By);
         const i64 Q1 = Cy * bx;
         const i64 cx = exact_div_r(Q1 - m, By, rBy, err);
         const i64 dx = exact_div_r(bx * Dy - w2, By, rBy, err);
+        (void)cx;
+        (void)dx;
         u3 = by * Cy;
-        w3 = bx * cx - G * dx;
-        v3 = v2 - 2 * Q1;
+        v3 = v2 - 2 * Q1;                  // (w3 = bx cx - G dx is not needed)
     }
     xo = x;
     yo = y;
 }
 
 // Algorithm 3 NUDUPL on the form (u, v, w).
-EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &w3, i64 &G, i64 &xo,
-                   i64 &yo, u32 *err) {
+EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &G, i64 &xo, i64 &yo,
+                   u32 *err) {
     i64 xx, yy;
     G = xgcd_s(u, v, xx, yy);     // xx u + yy v = G
     const i64 By = sdiv_exact23(u, G);
@@ -232,13 +268,10 @@ EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &w3, i64 &G
     i64 bx = Bx, by = By, x, y;
     int z;
     partial_euclid(bx, by, x, y, z, L);
-    const i64 ax = G * x, ay = G * y;
+    const i64 ay = G * y;
     if (z == 0) {
-        const i64 dx = exact_div(bx * Dy - w, By, err);
         u3 = by * by;
-        w3 = bx * bx;
-        v3 = v - (bx + by) * (bx + by) + u3 + w3;
-        w3 = w3 - G * dx;
+        v3 = v - (bx + by) * (bx + by) + u3 + bx * bx;   // (w3 update not needed)
     } else {
         const i64 dx = exact_div(bx * Dy - w * x, By, err);
         const i64 Q1 = dx * y;
@@ -246,10 +279,8 @@ EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &w3, i64 &G
         v3 = G * (dy + Q1);
         dy = exact_div(dy, x, err);
         u3 = by * by;
-        w3 = bx * bx;
-        v3 = v3 - (bx + by) * (bx + by) + u3 + w3;
-        u3 = u3 - ay * dy;
-        w3 = w3 - ax * dx;
+        v3 = v3 - (bx + by) * (bx + by) + u3 + bx * bx;
+        u3 = u3 - ay * dy;                               // (w3 update not needed)
     }
     xo = x;
     yo = y;
@@ -301,20 +332,20 @@ EIS_HD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 L, d
     const i64 Q1 = m1.Q, P1 = m1.P;
     P2 = P2 < Q2 ? P2 : floor_mod(P2, Q2);
     if (Q1 <= plain_th || Q2 <= plain_th) return plain_product(Q1, P1, Q2, P2, d, err);
-    i64 u3, v3, w3, G, x, y;
+    i64 u3, v3, G, x, y;
     Composed r;
     if (Q1 == Q2 && P1 == P2) {
-        nudupl(Q1 >> 1, -P1, m1.w, L, u3, v3, w3, G, x, y, err);
+        nudupl(Q1 >> 1, -P1, m1.w, L, u3, v3, G, x, y, err);
         r.kind = 2;
     } else {
         const i64 w2 = exact_div(P2 * P2 - d, 2 * Q2, err);
-        nucomp(Q1 >> 1, -P1, m1.w, Q2 >> 1, -P2, w2, L, u3, v3, w3, G, x, y, err);
+        nucomp(Q1 >> 1, -P1, m1.w, Q2 >> 1, -P2, w2, L, u3, v3, G, x, y, err);
         r.kind = 1;
     }
     r.Q = iabs64(2 * u3);
     r.P = floor_mod(-v3, r.Q);
     r.tg = t_gamma(x, y, v3);
-    r.lg = log2_gamma(G, x, y, u3, v3, sqrtd, Q1, Q2);
+    r.lg = log2_gamma(G, x, y, u3, v3, (float)sqrtd, Q1, Q2);
     if ((r.Q & 3) != 2 || (r.P & 1) != 1 || (G & 1) == 0) *err += 1;   // Thm A.1 / 2 inert
     return r;
 }
