@@ -289,6 +289,9 @@ EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &G, i64 &xo
 // Plain ideal product (the small-norm branch of Alg. 4, PAPER.md l.733, l.742-744;
 // the J-W Sec. 5.4 procedure is not reproduced in the paper: Dirichlet
 // composition, R20).  Inputs a_i = Q_i/2, b_i = P_i (odd).
+EIS_HD i64 mulmod(i64 a, i64 b, i64 M) {   // |a|, |b| < M < 2^31: (a b) mod M in [0, M)
+    return floor_mod(a * b, M);
+}
 EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
     const i64 a1 = Q1 >> 1, a2 = Q2 >> 1;
     i64 x, y;
@@ -296,16 +299,21 @@ EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
     const i64 n = (P1 + P2) / 2;
     i64 X, Y;
     const i64 S = xgcd_s(e, n, X, Y);         // X e + Y n = S
-    const i64 a3 = (a1 / S) * (a2 / S);
-    const __int128 num = (__int128)X * x * a1 * P2 + (__int128)X * y * a2 * P1 +
-                         (__int128)Y * (((__int128)P1 * P2 + d) / 2);
+    const i64 a3 = sdiv_exact23(a1, S) * sdiv_exact23(a2, S);
+    // b3 = num / S mod 2 a3 with num = X x a1 P2 + X y a2 P1 + Y (P1 P2 + d)/2;
+    // S | num, so reduce num modulo M = 2 a3 S (< 2^31: a1 <= 25) and divide.
+    const i64 M = 2 * a3 * S;
+    const i64 t1 = mulmod(mulmod(floor_mod(X, M), floor_mod(x, M), M),
+                          mulmod(a1, floor_mod(P2, M), M), M);
+    const i64 t2 = mulmod(mulmod(floor_mod(X, M), floor_mod(y, M), M),
+                          mulmod(a2, floor_mod(P1, M), M), M);
+    const i64 h = floor_mod(((P1 * P2) >> 1) + ((d >> 1) + 1) , M);   // (P1 P2 + d)/2, both odd
+    const i64 t3 = mulmod(floor_mod(Y, M), h, M);
+    const i64 num = floor_mod(t1 + t2 + t3, M);
     if (num % S != 0) *err += 1;
-    const __int128 M = 2 * (__int128)a3;
-    __int128 b3 = (num / S) % M;
-    if (b3 < 0) b3 += M;
     Composed r;
     r.Q = 2 * a3;
-    r.P = (i64)b3;
+    r.P = num / S;                             // in [0, 2 a3)
     r.tg = 0;                                  // gamma = S odd
     r.lg = log2_approx((float)S);
     r.kind = 0;
@@ -349,3 +357,150 @@ EIS_HD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 L, d
     if ((r.Q & 3) != 2 || (r.P & 1) != 1 || (G & 1) == 0) *err += 1;   // Thm A.1 / 2 inert
     return r;
 }
+
+// ---------------------------------------------------------------------------
+// NUCOMP, hot path of the giant kernel, in exact fp64 integer arithmetic.
+// Every quantity is an integer of magnitude < 2^53 at d <= 1e11 (<= 47 bits
+// measured), so DFMA/DMUL/DADD on them are exact; each
+// "without remainder" division is rint(n * rcp(dv)) with its remainder checked
+// by one exact DFMA (*err++ otherwise).  The Euclid loops run in exact FP32.
+// Same steps and variable names as nucomp() above (Alg. 2);
+// the rare branch F not | s (second xgcd) returns false and the caller uses the
+// int64 nucomp().
+EIS_HD double dexact_div(double n, double dv, double rdv, u32 *err) {
+    const double q = rint(n * rdv);
+    if (fma(-q, dv, n) != 0.0) *err += 1;
+    return q;
+}
+EIS_HD double dfloor_mod(double a, double b, double rb) {   // b > 0, result in [0, b)
+    const double q = floor(a * rb);
+    double r = fma(-q, b, a);
+    if (r < 0.0) r += b;
+    else if (r >= b) r -= b;
+    return r;
+}
+
+struct CompD {
+    double u3, v3, x, y, G;
+};
+
+EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, double w2, float L,
+                     CompD &o, u32 *err) {
+    if (w1 < w2) {
+        double t;
+        t = u1; u1 = u2; u2 = t;
+        t = v1; v1 = v2; v2 = t;
+        t = w1; w1 = w2; w2 = t;
+    }
+    const double s = (v1 + v2) * 0.5;          // exact: v1, v2 odd
+    const double m = v2 - s;
+    float fb;
+    const float F = fxgcd_x((float)u2, (float)u1, fb);   // b u2 = F (mod u1)
+    double G = 1.0, By = u1, Cy = u2, Dy = s;
+    if (F != 1.f) {
+        const float fs = fabsf((float)s);
+        if (fmaf(-ffloor_div_pos(fs, F), F, fs) != 0.f) return false;   // F does not divide s
+        G = (double)F;
+        const double rG = 1.0 / G;
+        By = rint(u1 * rG);
+        Cy = rint(u2 * rG);
+        Dy = rint(s * rG);
+    }
+    const double rBy = rcp64(By);
+    const double Bx = m * (double)fb;          // |m b| < 2^39
+    const float fbx0 = (float)dfloor_mod(Bx, By, rBy);
+    // partial Euclid (Alg. 2 l.637-643) in exact FP32
+    float fbx = fbx0, fby = (float)By, fx = 1.f, fy = 0.f;
+    int z = 0;
+    while (fby > L && fbx != 0.f) {
+        const float q = ffloor_div_pos(fby, fbx);
+        const float t = fmaf(-q, fbx, fby);
+        fby = fbx;
+        fbx = t;
+        const float u = fmaf(-q, fx, fy);
+        fy = fx;
+        fx = u;
+        z++;
+    }
+    if (z & 1) { fby = -fby; fy = -fy; }
+    const double bx = fbx, by = fby, x = fx, y = fy;
+    if (z != 0) {
+        const double cx = dexact_div(fma(Cy, bx, -m * x), By, rBy, err);
+        const double Q1 = by * cx;
+        const double Q2 = Q1 + m;
+        const double dx = dexact_div(fma(Dy, bx, -w2 * x), By, rBy, err);
+        const double Q3 = y * dx;
+        const double Q4 = Q3 + Dy;
+        const double dy = dexact_div(Q4, x, rcp64(x), err);
+        double cy;
+        if (bx != 0.0) cy = dexact_div(Q2, bx, rcp64(bx), err);
+        else cy = dexact_div(fma(cx, dy, -w1), dx, rcp64(dx), err);
+        o.u3 = fma(by, cy, -G * y * dy);
+        o.v3 = G * (Q3 + Q4) - Q1 - Q2;
+    } else {
+        const double Q1 = Cy * bx;
+        o.u3 = by * Cy;
+        o.v3 = v2 - 2.0 * Q1;
+    }
+    o.x = x;
+    o.y = y;
+    o.G = G;
+    return true;
+}
+
+// The giant step's composition (NUCOMPchoose, Alg. 4, for I1 = mu_1 and a reduced
+// I2 != mu_1) followed by the canonical representative (R17): returns
+// Q = |2 u3| and P* = s - ((s + v3) mod Q) in (s - Q, s] (P = -v3 mod Q, l.753).
+struct GiantComp {
+    i64 Q, P;
+    u32 tg, kind;
+    float lg;
+};
+
+EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, i64 L,
+                               float sqrtd_f, int plain_th, u32 *err) {
+    GiantComp r;
+    const i64 Q1 = m1.Q, P1 = m1.P;
+    if (P2 >= Q2) P2 -= Q2 * (i64)ffloor_div_pos((float)P2, (float)Q2);   // Alg. 4 l.739
+    if (Q1 <= plain_th || Q2 <= plain_th || (Q1 == Q2 && P1 == P2)) {
+        const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
+        r.Q = c.Q;
+        r.P = s - floor_mod(s - c.P, c.Q);
+        r.tg = c.tg;
+        r.lg = c.lg;
+        r.kind = c.kind;
+        return r;
+    }
+    const double dd = (double)d;
+    const double w2 = rint(((double)P2 * (double)P2 - dd) * rcp64(2.0 * (double)Q2));   // exact
+    CompD o;
+    if (!nucomp_d((double)(Q1 >> 1), -(double)P1, (double)m1.w, (double)(Q2 >> 1), -(double)P2,
+                  w2, (float)L, o, err)) {
+        const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
+        r.Q = c.Q;
+        r.P = s - floor_mod(s - c.P, c.Q);
+        r.tg = c.tg;
+        r.lg = c.lg;
+        r.kind = c.kind;
+        return r;
+    }
+    const double Qd = fabs(2.0 * o.u3);
+    const double sd = (double)s;
+    const double Ps = sd - dfloor_mod(sd + o.v3, Qd, rcp64(Qd));
+    r.Q = (i64)Qd;
+    r.P = (i64)Ps;
+    // t(gamma) = DLOG[(x + y (v3-1)/2) mod 2][y mod 2] (R12)
+    const i64 xi = (i64)o.x, yi = (i64)o.y, v3i = (i64)o.v3;
+    r.tg = t_gamma(xi, yi, v3i);
+    // log2|gamma|, gamma = G (a + y sqrt d)/(2 u3), a = 2 x u3 + y v3
+    const double a = fma(2.0 * o.x, o.u3, o.y * o.v3);
+    const float mag = fabsf((float)a) + fabsf((float)o.y) * sqrtd_f;
+    if ((a >= 0.0) == (o.y >= 0.0) || a == 0.0 || o.y == 0.0)
+        r.lg = log2_approx((float)o.G * mag / (float)Qd);
+    else   // |N(gamma)| = (Q1/2)(Q2/2)/|u3|, use the conjugate (no cancellation)
+        r.lg = log2_approx(2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1) / ((float)o.G * mag));
+    r.kind = 1;
+    if (((r.Q & 3) != 2) | ((r.P & 1) != 1) | (((i64)o.G & 1) == 0)) *err += 1;
+    return r;
+}
+

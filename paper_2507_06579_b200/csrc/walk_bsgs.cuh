@@ -232,22 +232,21 @@ EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u64 *tab, const BsgsArgs &B, u32
     GiantInfo gi;
     const i64 d = (i64)g.d;
     const i64 s = g.s;
-    const Composed c = nucomp_choose(g.m1, (i64)g.Qc, (i64)g.Pc, d, g.L, g.sqrtd, B.plain_th, err);
+    const GiantComp c = giant_compose(g.m1, (i64)g.Qc, (i64)g.Pc, d, s, g.L, (float)g.sqrtd,
+                                      B.plain_th, err);
     gi.kind = c.kind;
     u32 t = mod3(g.t1 + g.tc + 3u - c.tg);       // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
     float dist = g.dist1 + g.distc - c.lg;
-    i64 Q = c.Q, P = c.P;
+    i64 Q = c.Q, P = c.P;                        // P canonical in (s - Q, s]
     u32 nred = 0;
-    for (;;) {
-        P = s - floor_mod(s - P, Q);                // canonical P in (s - Q, s]
-        if (Q - P <= s) break;                      // reduced (R18)
+    while (Q - P > s) {                          // not reduced (R18): apply rho
         const i64 q = floor_div(P + s, Q);          // floor((P + sqrt d)/Q)
         const i64 Pn = q * Q - P;
         const i64 Qn = exact_div(d - Pn * Pn, Q, err);
         t = mod3(t + 1u + (u32)((Pn >> 1) & 1));
         dist += log2_approx((float)fabs((double)Pn + g.sqrtd)) - log2_approx((float)Q);
-        P = Pn;
         Q = iabs64(Qn);
+        P = s - floor_mod(s - Pn, Q);               // canonical P in (s - Q, s]
         if (++nred > 4096) { *err += 1; break; }
     }
     gi.nred = nred;
