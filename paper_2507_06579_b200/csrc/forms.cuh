@@ -364,9 +364,8 @@ EIS_HD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 L, d
 // measured), so DFMA/DMUL/DADD on them are exact; each
 // "without remainder" division is rint(n * rcp(dv)) with its remainder checked
 // by one exact DFMA (*err++ otherwise).  The Euclid loops run in exact FP32.
-// Same steps and variable names as nucomp() above (Alg. 2);
-// the rare branch F not | s (second xgcd) returns false and the caller uses the
-// int64 nucomp().
+// Same steps and variable names as nucomp() above (Alg. 2),
+// including the branch F not | s (second xgcd, products reduced mod H first).
 EIS_HD double dexact_div(double n, double dv, double rdv, u32 *err) {
     const double q = rint(n * rdv);
     if (fma(-q, dv, n) != 0.0) *err += 1;
@@ -396,19 +395,36 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     const double m = v2 - s;
     float fb;
     const float F = fxgcd_x((float)u2, (float)u1, fb);   // b u2 = F (mod u1)
-    double G = 1.0, By = u1, Cy = u2, Dy = s;
-    if (F != 1.f) {
+    double G = 1.0, By = u1, Cy = u2, Dy = s, rBy;
+    float fbx0;
+    if (F == 1.f) {                            // gcd(u1, u2) = 1: G = 1, Bx = m b
+        rBy = rcp64(By);
+        fbx0 = (float)dfloor_mod(m * (double)fb, By, rBy);      // |m b| < 2^39
+    } else {
         const float fs = fabsf((float)s);
-        if (fmaf(-ffloor_div_pos(fs, F), F, fs) != 0.f) return false;   // F does not divide s
-        G = (double)F;
-        const double rG = 1.0 / G;
+        float fyy;
+        const float Gf = fxgcd_x(fs, F, fyy);  // yy |s| = G (mod F)
+        G = (double)Gf;
+        const double rG = rcp64(G);
         By = rint(u1 * rG);
         Cy = rint(u2 * rG);
         Dy = rint(s * rG);
+        rBy = rcp64(By);
+        if (Gf == F) {                         // F | s: G = F, Bx = m b
+            fbx0 = (float)dfloor_mod(m * (double)fb, By, rBy);
+        } else {                               // Alg. 2 l.630-634, all reduced mod H first
+            const double H = rint((double)F * rG), rH = rcp64(H);
+            const double b = fb;
+            const double c = dexact_div(fma(-b, u2, (double)F), u1, rcp64(u1), err);
+            const double yy = s < 0.0 ? -(double)fyy : (double)fyy;
+            const double inner = dfloor_mod(
+                fma(dfloor_mod(b, H, rH), dfloor_mod(w1, H, rH),
+                    dfloor_mod(c, H, rH) * dfloor_mod(w2, H, rH)), H, rH);
+            const double l = dfloor_mod(dfloor_mod(yy, H, rH) * inner, H, rH);
+            const double Bx = dexact_div(fma(b, m, l * By), H, rH, err);
+            fbx0 = (float)dfloor_mod(Bx, By, rBy);
+        }
     }
-    const double rBy = rcp64(By);
-    const double Bx = m * (double)fb;          // |m b| < 2^39
-    const float fbx0 = (float)dfloor_mod(Bx, By, rBy);
     // partial Euclid (Alg. 2 l.637-643) in exact FP32
     float fbx = fbx0, fby = (float)By, fx = 1.f, fy = 0.f;
     int z = 0;
