@@ -177,7 +177,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     u64 seg_cap = SEG;
     if (bsgs) {
         const int nsl = bsgs_ns_log2(cand_d(i_last), g.alpha_x16 / 16.0f);
-        const u64 per = ((u64)8 << nsl) + ((u64)4 << nsl) / 32 + sizeof(GiantRec) + 4;
+        const u64 per = ((u64)4 << nsl) + ((u64)4 << nsl) / 2 + sizeof(GiantRec) + 4;
         seg_cap = std::min<u64>(SEG, std::max<u64>((16ull << 30) / per, 1ull << 16));
     }
     for (u64 seg = i_first; seg <= i_last;) {

@@ -53,27 +53,32 @@ struct BsgsArgs {
 };
 
 // ---------------------------------------------------------------- the store --
+// Per d: a hash table of u32 slots keyed on Q, slot = (Q >> 2) | (j + 1) << 18 |
+// t << 28 (Q = 2 mod 4 and Q < 2^20, so Q >> 2 < 2^18 is exact; j < 1023 is the
+// entry's index in insertion order; t = t(theta) mod 3), plus a dense list
+// written in insertion order, list[j] = P | (2 log2 theta) << 19 (P < 2^19).
+// Same-Q entries share a probe chain and are told apart by P from the list.
 struct Store {
     u32 *bm;            // occupancy bits: word w at bm[w * stride]
     int stride;
-    u64 *tab;           // slots of this d
+    u32 *tab;           // slots of this d
+    u32 *list;          // entries of this d in insertion order
     int ns_log2;
 };
 
-EIS_HD u32 store_hash(u32 Q, u32 P, int ns_log2) {
-    return ((Q * 0x9E3779B1u) ^ (P * 0x85EBCA77u)) >> (32 - ns_log2);
-}
+EIS_HD u32 store_hash(u32 Q, int ns_log2) { return (Q * 0x9E3779B1u) >> (32 - ns_log2); }
 
 EIS_HD void store_clear(Store &S) {
     for (int w = 0; w < (1 << S.ns_log2) / 32; w++) S.bm[w * S.stride] = 0;
 }
 
-EIS_HD void store_insert(Store &S, u32 Q, u32 P, u32 traw, float dist2) {
+EIS_HD void store_insert(Store &S, u32 j, u32 Q, u32 P, u32 t3, float dist2) {
     const u32 mask = (1u << S.ns_log2) - 1;
-    u32 h = store_hash(Q, P, S.ns_log2);
+    u32 h = store_hash(Q, S.ns_log2);
     const float fx = dist2 * 2.0f;
-    const u64 dfx = fx <= 0.f ? 0 : (fx >= 8191.f ? 8191ull : (u64)fx);   // floor, 0.5 units
-    const u64 e = (u64)Q | ((u64)P << 20) | ((u64)(traw & 2047u) << 40) | (dfx << 51);
+    const u32 dfx = fx <= 0.f ? 0u : (fx >= 8191.f ? 8191u : (u32)fx);   // floor, 0.5 units
+    S.list[j] = P | (dfx << 19);
+    const u32 e = (Q >> 2) | ((j + 1) << 18) | (t3 << 28);
     for (;;) {
         u32 *wp = &S.bm[(h >> 5) * S.stride];
         const u32 w = *wp;
@@ -88,15 +93,25 @@ EIS_HD void store_insert(Store &S, u32 Q, u32 P, u32 traw, float dist2) {
     }
 }
 
-// returns the entry or 0.  Stores are zero-filled before use (an entry is never
-// 0: Q >= 2), so probing stops at the first empty slot without the bitmap.
-EIS_HD u64 store_lookup(const u64 *tab, int ns_log2, u32 Q, u32 P) {
+// Look (Q, P) up.  Tables are zero-filled before use (a slot is never 0: j+1 >= 1),
+// so probing stops at the first empty slot.  Returns true with t3 and the
+// stored log2 distance on a hit.
+EIS_HD bool store_lookup(const u32 *tab, const u32 *list, int ns_log2, u32 Q, u32 P, u32 &t3,
+                         float &dist2) {
     const u32 mask = (1u << ns_log2) - 1;
-    const u64 key = (u64)Q | ((u64)P << 20);
-    u32 h = store_hash(Q, P, ns_log2);
+    const u32 qk = Q >> 2;
+    u32 h = store_hash(Q, ns_log2);
     for (;;) {
-        const u64 e = tab[h];
-        if (e == 0 || (e & 0xFFFFFFFFFFull) == key) return e;
+        const u32 e = tab[h];
+        if (e == 0) return false;
+        if ((e & 0x3FFFFu) == qk) {
+            const u32 le = list[((e >> 18) & 1023u) - 1];
+            if ((le & 0x7FFFFu) == P) {
+                t3 = e >> 28;
+                dist2 = (float)(le >> 19) * 0.5f;
+                return true;
+            }
+        }
         h = (h + 1) & mask;
     }
 }
@@ -149,10 +164,10 @@ EIS_HD bool bsgs_begin(BsgsLane &ln, Store &S, const BsgsArgs &B, u64 d) {
     }
     store_clear(S);
     // theta_1 = 1 <-> (2, P*) with P* the odd representative in (s-2, s] = P_1
-    store_insert(S, 2u, ln.st.P, 0u, 0.f);
+    store_insert(S, 0u, 2u, ln.st.P, 0u, 0.f);
     // theta_2 = ((P_1 + sqrt d)/2) theta_1 <-> (Q_1, P_1)
     ln.dist = log2_approx(((float)ln.st.P + ln.sqrtd_f) * 0.5f);
-    store_insert(S, ln.st.Q, ln.st.P, ln.st.t2 >> 1, ln.dist);
+    store_insert(S, 1u, ln.st.Q, ln.st.P, mod3(ln.st.t2 >> 1), ln.dist);
     ln.n_ent = 2;
     ln.extras = -1;
     ln.phase = PH_BABY;
@@ -176,7 +191,7 @@ EIS_HD int bsgs_baby(BsgsLane &ln, Store &S, const BsgsArgs &B, int kmax) {
             return k;
         }
         const bool ex = rho_step_dist(ln.st, ln.sqrtd_f, ln.dist);
-        store_insert(S, ln.st.Q, ln.st.P, ln.st.t2 >> 1, ln.dist);
+        store_insert(S, (u32)ln.n_ent, ln.st.Q, ln.st.P, mod3(ln.st.t2 >> 1), ln.dist);
         ln.n_ent++;
         if (ex) {
             ln.res = baby_result(ln.st);
@@ -228,7 +243,8 @@ struct GiantInfo {
 
 // One giant step.  Sets PH_DONE on a guarded hit, PH_HALF
 // when the cap is exceeded.  *err counts invariant violations.
-EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u64 *tab, const BsgsArgs &B, u32 *err) {
+EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u32 *tab, const u32 *list, const BsgsArgs &B,
+                            u32 *err) {
     GiantInfo gi;
     const i64 d = (i64)g.d;
     const i64 s = g.s;
@@ -251,15 +267,12 @@ EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u64 *tab, const BsgsArgs &B, u32
     }
     gi.nred = nred;
     g.k++;
-    const u64 e = store_lookup(tab, B.ns_log2, (u32)Q, (u32)P);
-    if (e) {
-        const float de = (float)(e >> 51) * 0.5f;
-        if (dist - de >= GUARD_LOG2) {
-            const u32 te = mod3((u32)((e >> 40) & 2047u));
-            g.res = mod3(t + 3u - te);              // eps = mu'_k / theta
-            g.phase = PH_DONE;
-            return gi;
-        }
+    u32 te;
+    float de;
+    if (store_lookup(tab, list, B.ns_log2, (u32)Q, (u32)P, te, de) && dist - de >= GUARD_LOG2) {
+        g.res = mod3(t + 3u - te);                  // eps = mu'_k / theta
+        g.phase = PH_DONE;
+        return gi;
     }
     g.Qc = (u32)Q;
     g.Pc = (u32)P;
@@ -277,7 +290,9 @@ struct __align__(32) GiantRec {
 };
 
 struct BsgsOut {
-    u64 *tables;        // [segment survivors][ns] store slots
+    u32 *tables;        // [segment survivors][ns] store slots
+    u32 *lists;         // [segment survivors][lcap] store entries
+    int lcap;
     GiantRec *recs;     // [segment survivors]
     u32 *queue;         // survivor indices needing giant steps
     u32 *qcount;        // device: queue length
@@ -351,9 +366,9 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         base = __shfl_sync(FULL_MASK, base, 0);
         if (base >= n) break;
         const u32 idx = base + lane;
-        {   // zero the batch's 32 contiguous stores (coalesced, full lines)
+        {   // zero the batch's 32 contiguous tables (coalesced, full lines)
             uint4 *z = reinterpret_cast<uint4 *>(o.tables + ((u64)base << B.ns_log2));
-            const u32 nz = (min(n - base, 32u) << B.ns_log2) / 2;
+            const u32 nz = (min(n - base, 32u) << B.ns_log2) / 4;
             const uint4 zero = make_uint4(0, 0, 0, 0);
             for (u32 c = lane; c < nz; c += 32) z[c] = zero;
             __syncwarp();
@@ -364,6 +379,7 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         if (idx < n) {
             off = __ldg(a.list + idx);
             S.tab = o.tables + ((u64)idx << B.ns_log2);
+            S.list = o.lists + (u64)idx * o.lcap;
             baby += 1;
             if (bsgs_begin(ln, S, B, cand_d(a.i0 + off))) {
                 record_result(a, hist, off, ln.d, ln.res);
@@ -388,7 +404,7 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         if (ln.phase == PH_GIANT) {
             GiantLane g;
             giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
-            const GiantInfo gi = bsgs_giant(g, S.tab, B, &err);
+            const GiantInfo gi = bsgs_giant(g, S.tab, S.list, B, &err);
             giant++;
             red += gi.nred;
             if (g.phase == PH_DONE) {
@@ -429,7 +445,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 
     const int lane = threadIdx.x & 31;
     const u32 nq = *o.qcount;
-    const u64 *tab = nullptr;
+    const u32 *tab = nullptr, *list = nullptr;
     GiantLane g;
     g.phase = PH_IDLE;
     u32 off = 0;
@@ -457,6 +473,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                     g.k = (int)(r.tk >> 4);
                     g.distc = r.distc;
                     tab = o.tables + ((u64)idx << B.ns_log2);
+                    list = o.lists + (u64)idx * o.lcap;
                 } else {
                     exhausted = true;
                 }
@@ -464,7 +481,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         if (__all_sync(FULL_MASK, exhausted && g.phase == PH_IDLE)) break;
         if (g.phase == PH_GIANT) {
-            const GiantInfo gi = bsgs_giant(g, tab, B, &err);
+            const GiantInfo gi = bsgs_giant(g, tab, list, B, &err);
             giant++;
             red += gi.nred;
             if (g.phase == PH_HALF) {     // cap exceeded: exact half walk instead
@@ -492,8 +509,10 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 
 // ------------------------------------------------------------- host launch --
 struct BsgsScratch {
-    u64 *tables = nullptr;
+    u32 *tables = nullptr;
     size_t tables_bytes = 0;
+    u32 *lists = nullptr;
+    size_t lists_n = 0;
     GiantRec *recs = nullptr;
     size_t recs_n = 0;
     u32 *queue = nullptr;
@@ -502,6 +521,7 @@ struct BsgsScratch {
 
 inline void bsgs_free(BsgsScratch &s) {
     if (s.tables) cudaFree(s.tables);
+    if (s.lists) cudaFree(s.lists);
     if (s.recs) cudaFree(s.recs);
     if (s.queue) cudaFree(s.queue);
     s = BsgsScratch();
@@ -513,7 +533,10 @@ constexpr int BSGS_THREADS = 256;
 // store size for a segment whose largest d is d_max (load <= 1/2)
 inline int bsgs_ns_log2(u64 d_max, float alpha) {
     const double w = alpha * std::pow((double)d_max, 0.25);   // window in nats
-    const double need = 2.0 * (w / 1.1 + 8.0);                // ~1.2 nats per baby step
+    // ~1.22 nats per baby step: the window needs ~w/1.22 entries;
+    // size for load <= 1/2 at 95% of that (the cap ends the window a little
+    // early for the longest walks, which only adds giant steps).
+    const double need = 2.0 * 0.95 * (w / 1.22) + 8.0;
     int l = 6;
     while ((double)(1 << l) < need && l < 10) l++;
     return l;
@@ -543,10 +566,14 @@ inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, in
     size_t tb = scr.tables_bytes;
     if (bsgs_grow(scr.tables, tb, (n + 32) << B.ns_log2)) return -3;   // +32: batch tail
     scr.tables_bytes = tb;
+    const int lcap = (B.cap + 2 + 31) & ~31;
+    if (bsgs_grow(scr.lists, scr.lists_n, n * (size_t)lcap)) return -3;
     if (bsgs_grow(scr.recs, scr.recs_n, n)) return -3;
     if (bsgs_grow(scr.queue, scr.queue_n, n)) return -3;
     BsgsOut o;
     o.tables = scr.tables;
+    o.lists = scr.lists;
+    o.lcap = lcap;
     o.recs = scr.recs;
     o.queue = scr.queue;
     o.qcount = qctr;
@@ -556,7 +583,7 @@ inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, in
     // Baby kernel: the stores being filled are written at random slots; keep
     // the resident ones within L2 (~80 MB of 126 MB) so partially written
     // sectors never go to DRAM (measured: 2x DRAM read-modify-write otherwise).
-    const size_t store_bytes = (size_t)8 << B.ns_log2;
+    const size_t store_bytes = (size_t)4 << B.ns_log2;
     int bt = 256;
     while (bt > 32 && (size_t)num_sms * bt * store_bytes > ((size_t)80 << 20)) bt >>= 1;
     const size_t smem = (size_t)(2 * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * bt * 4;

@@ -25,7 +25,7 @@ int main(int argc, char **argv) {
     B.plain_th = argc > 4 ? atoi(argv[4]) : 50;
     B.giant_cap_mul = 20.0f;
     std::vector<u32> bm(1 << 10);
-    std::vector<u64> tab(1 << 14);
+    std::vector<u32> tab(1 << 14), lst(1 << 13);
     unsigned long long d;
     while (scanf("%llu", &d) == 1) {
         u32 res = 0, err = 0;
@@ -46,8 +46,9 @@ int main(int argc, char **argv) {
             S.bm = bm.data();
             S.stride = 1;
             S.tab = tab.data();
+            S.list = lst.data();
             S.ns_log2 = B.ns_log2;
-            std::fill(tab.begin(), tab.begin() + (1 << B.ns_log2), 0ull);
+            std::fill(tab.begin(), tab.begin() + (1 << B.ns_log2), 0u);
             BsgsLane ln;
             baby = 1;
             bsgs_begin(ln, S, B, d);
@@ -58,7 +59,7 @@ int main(int argc, char **argv) {
                 GiantLane g;
                 giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
                 while (g.phase == PH_GIANT) {
-                    GiantInfo gi = bsgs_giant(g, S.tab, B, &err);
+                    GiantInfo gi = bsgs_giant(g, S.tab, S.list, B, &err);
                     giant++;
                     red += gi.nred;
                     kinds[gi.kind]++;
