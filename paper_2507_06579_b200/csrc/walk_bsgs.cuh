@@ -66,6 +66,14 @@ struct Store {
     int ns_log2;
 };
 
+EIS_HD void store_streaming(u32 *p, u32 v) {
+#ifdef __CUDA_ARCH__
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 EIS_HD u32 store_hash(u32 Q, int ns_log2) { return (Q * 0x9E3779B1u) >> (32 - ns_log2); }
 
 EIS_HD void store_clear(Store &S) {
@@ -77,7 +85,7 @@ EIS_HD void store_insert(Store &S, u32 j, u32 Q, u32 P, u32 t3, float dist2) {
     u32 h = store_hash(Q, S.ns_log2);
     const float fx = dist2 * 2.0f;
     const u32 dfx = fx <= 0.f ? 0u : (fx >= 8191.f ? 8191u : (u32)fx);   // floor, 0.5 units
-    S.list[j] = P | (dfx << 19);
+    store_streaming(&S.list[j], P | (dfx << 19));   // evict-first: keep the tables in L2
     const u32 e = (Q >> 2) | ((j + 1) << 18) | (t3 << 28);
     for (;;) {
         u32 *wp = &S.bm[(h >> 5) * S.stride];
@@ -94,15 +102,15 @@ EIS_HD void store_insert(Store &S, u32 j, u32 Q, u32 P, u32 t3, float dist2) {
 }
 
 // Look (Q, P) up.  Tables are zero-filled before use (a slot is never 0: j+1 >= 1),
-// so probing stops at the first empty slot.  Returns true with t3 and the
-// stored log2 distance on a hit.
-EIS_HD bool store_lookup(const u32 *tab, const u32 *list, int ns_log2, u32 Q, u32 P, u32 &t3,
-                         float &dist2) {
+// so probing stops at the first empty slot.  Split in two so the giant kernel
+// can issue the first probe load, compute the next giant step, and only then
+// resolve the probe (the next step does not depend on the lookup).
+// Returns true with t3 and the stored log2 distance on a hit.
+EIS_HD bool store_resolve(const u32 *tab, const u32 *list, int ns_log2, u32 h, u32 e, u32 Q,
+                          u32 P, u32 &t3, float &dist2) {
     const u32 mask = (1u << ns_log2) - 1;
     const u32 qk = Q >> 2;
-    u32 h = store_hash(Q, ns_log2);
     for (;;) {
-        const u32 e = tab[h];
         if (e == 0) return false;
         if ((e & 0x3FFFFu) == qk) {
             const u32 le = list[((e >> 18) & 1023u) - 1];
@@ -113,7 +121,13 @@ EIS_HD bool store_lookup(const u32 *tab, const u32 *list, int ns_log2, u32 Q, u3
             }
         }
         h = (h + 1) & mask;
+        e = tab[h];
     }
+}
+EIS_HD bool store_lookup(const u32 *tab, const u32 *list, int ns_log2, u32 Q, u32 P, u32 &t3,
+                         float &dist2) {
+    const u32 h = store_hash(Q, ns_log2);
+    return store_resolve(tab, list, ns_log2, h, tab[h], Q, P, t3, dist2);
 }
 
 EIS_HD u32 mod3(u32 v) { return v % 3u; }
@@ -241,10 +255,9 @@ struct GiantInfo {
     u32 nred;       // rho steps in the reduction
 };
 
-// One giant step.  Sets PH_DONE on a guarded hit, PH_HALF
-// when the cap is exceeded.  *err counts invariant violations.
-EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u32 *tab, const u32 *list, const BsgsArgs &B,
-                            u32 *err) {
+// Advance: mu'_k = rho-reduce(NUCOMPchoose(mu_1, mu'_{k-1})) with its residue and
+// distance; no lookup.  *err counts invariant violations.
+EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err) {
     GiantInfo gi;
     const i64 d = (i64)g.d;
     const i64 s = g.s;
@@ -267,17 +280,35 @@ EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u32 *tab, const u32 *list, const
     }
     gi.nred = nred;
     g.k++;
-    u32 te;
-    float de;
-    if (store_lookup(tab, list, B.ns_log2, (u32)Q, (u32)P, te, de) && dist - de >= GUARD_LOG2) {
-        g.res = mod3(t + 3u - te);                  // eps = mu'_k / theta
-        g.phase = PH_DONE;
-        return gi;
-    }
     g.Qc = (u32)Q;
     g.Pc = (u32)P;
     g.tc = t;
     g.distc = dist;
+    return gi;
+}
+
+// Lookup verdict for a giant-step result (Q, P, t, dist):
+// a stored theta with log mu'_k - log theta >= 1 gives t(eps) = t - t(theta).
+EIS_HD bool giant_hit(u32 te, float de, u32 t, float dist, u32 &res) {
+    if (dist - de >= GUARD_LOG2) {
+        res = mod3(t + 3u - te);                    // eps = mu'_k / theta
+        return true;
+    }
+    return false;
+}
+
+// One unpipelined giant step (advance + lookup): used for k = 2 in the baby
+// kernel and by the CPU emulation.  Sets PH_DONE on a hit, PH_HALF past the cap.
+EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u32 *tab, const u32 *list, const BsgsArgs &B,
+                            u32 *err) {
+    const GiantInfo gi = giant_advance(g, B, err);
+    u32 te;
+    float de;
+    if (store_lookup(tab, list, B.ns_log2, g.Qc, g.Pc, te, de) &&
+        giant_hit(te, de, g.tc, g.distc, g.res)) {
+        g.phase = PH_DONE;
+        return gi;
+    }
     if (g.k > g.kcap) g.phase = PH_HALF;
     return gi;
 }
@@ -449,7 +480,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     GiantLane g;
     g.phase = PH_IDLE;
     u32 off = 0;
-    bool exhausted = false;
+    bool exhausted = false, pending = false;
     u64 baby = 0, giant = 0, red = 0, done = 0, fb = 0;
     u32 err = 0;
 
@@ -472,6 +503,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                     g.tc = (r.tk >> 2) & 3u;
                     g.k = (int)(r.tk >> 4);
                     g.distc = r.distc;
+                    pending = false;              // mu'_2 was checked by the baby kernel
                     tab = o.tables + ((u64)idx << B.ns_log2);
                     list = o.lists + (u64)idx * o.lcap;
                 } else {
@@ -481,9 +513,27 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         if (__all_sync(FULL_MASK, exhausted && g.phase == PH_IDLE)) break;
         if (g.phase == PH_GIANT) {
-            const GiantInfo gi = bsgs_giant(g, tab, list, B, &err);
+            // software pipeline: probe mu'_k (queued on refill already checked
+            // for k = 2: `pending` false) while computing mu'_{k+1}
+            const u32 pQ = g.Qc, pP = g.Pc, pt = g.tc;
+            const float pdist = g.distc;
+            u32 h = 0, e0 = 0;
+            if (pending) {
+                h = store_hash(pQ, B.ns_log2);
+                e0 = tab[h];
+            }
+            const GiantInfo gi = giant_advance(g, B, &err);
             giant++;
             red += gi.nred;
+            u32 te;
+            float de;
+            if (pending && store_resolve(tab, list, B.ns_log2, h, e0, pQ, pP, te, de) &&
+                giant_hit(te, de, pt, pdist, g.res)) {
+                g.phase = PH_DONE;
+            } else if (g.k > g.kcap) {
+                g.phase = PH_HALF;
+            }
+            pending = true;
             if (g.phase == PH_HALF) {     // cap exceeded: exact half walk instead
                 fb++;
                 BabyState st;
