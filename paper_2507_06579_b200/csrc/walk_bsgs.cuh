@@ -190,8 +190,14 @@ EIS_HD bool bsgs_begin(BsgsLane &ln, Store &S, const BsgsArgs &B, u64 d) {
 
 // Up to `kmax` baby steps.  Sets ln.phase to PH_DONE (symmetry exit) or
 // PH_GIANT (window complete).  Returns the number of rho steps taken.
+// Software-pipelined: the store insert of entry j (a shared-memory
+// read-modify-write chain) is issued after the rho step j+1, so the two
+// dependency chains overlap; the pending entry is flushed before returning.
 EIS_HD int bsgs_baby(BsgsLane &ln, Store &S, const BsgsArgs &B, int kmax) {
     int k = 0;
+    bool have = false;
+    u32 pj = 0, pQ = 0, pP = 0, pt = 0;
+    float pd = 0.f;
     for (; k < kmax; k++) {
         if (ln.extras < 0 && (ln.dist >= ln.W2 || ln.n_ent >= B.cap)) {
             ln.Q1 = ln.st.Q;                 // mu_1 = theta_j
@@ -202,18 +208,26 @@ EIS_HD int bsgs_baby(BsgsLane &ln, Store &S, const BsgsArgs &B, int kmax) {
         }
         if (ln.extras == 0) {
             ln.phase = PH_GIANT;
-            return k;
+            break;
         }
         const bool ex = rho_step_dist(ln.st, ln.sqrtd_f, ln.dist);
-        store_insert(S, (u32)ln.n_ent, ln.st.Q, ln.st.P, mod3(ln.st.t2 >> 1), ln.dist);
+        if (have) store_insert(S, pj, pQ, pP, pt, pd);
+        pj = (u32)ln.n_ent;
+        pQ = ln.st.Q;
+        pP = ln.st.P;
+        pt = mod3(ln.st.t2 >> 1);
+        pd = ln.dist;
+        have = true;
         ln.n_ent++;
         if (ex) {
             ln.res = baby_result(ln.st);
             ln.phase = PH_DONE;
-            return k + 1;
+            k++;
+            break;
         }
         if (ln.extras > 0) ln.extras--;
     }
+    if (have) store_insert(S, pj, pQ, pP, pt, pd);
     return k;
 }
 
@@ -430,30 +444,26 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 }
             }
         }
-        // k = 2 for all lanes together: mu_2 = mu_1 * mu_1 (NUDUPL)
+        // k = 2 for all lanes together: mu_2 = mu_1 * mu_1 (NUDUPL).  Its lookup
+        // is left to the giant kernel's pipelined probe (no memory wait here).
         bool push = false;
         if (ln.phase == PH_GIANT) {
             GiantLane g;
             giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
-            const GiantInfo gi = bsgs_giant(g, S.tab, S.list, B, &err);
+            const GiantInfo gi = giant_advance(g, B, &err);
             giant++;
             red += gi.nred;
-            if (g.phase == PH_DONE) {
-                record_result(a, hist, off, ln.d, g.res);
-                done++;
-            } else {
-                GiantRec r;
-                r.off = off;
-                r.Q1 = ln.Q1;
-                r.P1 = ln.P1;
-                r.Qc = g.Qc;
-                r.Pc = g.Pc;
-                r.tk = g.t1 | (g.tc << 2) | ((u32)g.k << 4);
-                r.dist1 = g.dist1;
-                r.distc = g.distc;
-                o.recs[idx] = r;
-                push = true;
-            }
+            GiantRec r;
+            r.off = off;
+            r.Q1 = ln.Q1;
+            r.P1 = ln.P1;
+            r.Qc = g.Qc;
+            r.Pc = g.Pc;
+            r.tk = g.t1 | (g.tc << 2) | ((u32)g.k << 4);
+            r.dist1 = g.dist1;
+            r.distc = g.distc;
+            o.recs[idx] = r;
+            push = true;
         }
         const u32 pm = __ballot_sync(FULL_MASK, push);
         if (pm) {
@@ -503,7 +513,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                     g.tc = (r.tk >> 2) & 3u;
                     g.k = (int)(r.tk >> 4);
                     g.distc = r.distc;
-                    pending = false;              // mu'_2 was checked by the baby kernel
+                    pending = true;               // mu'_2 is probed with the next advance
                     tab = o.tables + ((u64)idx << B.ns_log2);
                     list = o.lists + (u64)idx * o.lcap;
                 } else {
