@@ -89,8 +89,13 @@ EIS_API void eis_finalize(void);
  * the library, valid until the next call. */
 EIS_API const char *eis_last_error(void);
 
-/* Tunables (keys: "mode", "crossover", "alpha_x16", "segment_log2",
- * "blocks_per_sm", "threads"); unknown key or bad value -> EIS_EINVAL. */
+/* Tunables; unknown key or bad value -> EIS_EINVAL.  None changes a result.
+ *  "mode"          EIS_MODE_* (default AUTO)
+ *  "crossover"     AUTO: HALF for segments starting below this d, else BSGS
+ *  "alpha_x16"     BSGS baby window W = (alpha_x16/16) d^(1/4), in [4, 64]
+ *  "segment_log2"  candidates per segment (HALF; BSGS caps it by store memory)
+ *  "blocks_per_sm" HALF walk kernel CTAs per SM
+ *  "baby_l2_mb"    BSGS baby kernel: MB of L2 its resident stores may occupy */
 EIS_API int eis_set_option(const char *key, int64_t value);
 EIS_API int64_t eis_get_option(const char *key);
 

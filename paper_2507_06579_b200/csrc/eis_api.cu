@@ -50,6 +50,7 @@ struct Ctx {
     int segment_log2 = 25;
     int blocks_per_sm = 8;
     int threads = 256;
+    int baby_l2_mb = 40;
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
@@ -229,8 +230,8 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.stats = g.d_stats;
         CUDA_TRY(cudaEventRecord(g.ev[2], s));
         if (bsgs) {
-            int rc = launch_bsgs(a, len, d_last, g.num_sms, g.alpha_x16, g.bsgs, g.d_ctr + 3, s,
-                                 &g.launches);
+            int rc = launch_bsgs(a, len, d_last, g.num_sms, g.alpha_x16, g.baby_l2_mb, g.bsgs,
+                                 g.d_ctr + 3, s, &g.launches);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS launch failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -353,6 +354,7 @@ void eis_finalize(void) {
     fresh.alpha_x16 = g.alpha_x16;
     fresh.segment_log2 = g.segment_log2;
     fresh.blocks_per_sm = g.blocks_per_sm;
+    fresh.baby_l2_mb = g.baby_l2_mb;
     g = fresh;
 }
 
@@ -373,6 +375,9 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "segment_log2") {
         if (v < 18 || v > 31) return fail(EIS_EINVAL, "segment_log2 must be in [18, 31]");
         g.segment_log2 = (int)v;
+    } else if (k == "baby_l2_mb") {
+        if (v < 1 || v > 4096) return fail(EIS_EINVAL, "baby_l2_mb must be in [1, 4096]");
+        g.baby_l2_mb = (int)v;
     } else if (k == "blocks_per_sm") {
         if (v < 1 || v > 32) return fail(EIS_EINVAL, "blocks_per_sm must be in [1, 32]");
         g.blocks_per_sm = (int)v;
@@ -390,6 +395,7 @@ int64_t eis_get_option(const char *key) {
     if (k == "alpha_x16") return g.alpha_x16;
     if (k == "segment_log2") return g.segment_log2;
     if (k == "blocks_per_sm") return g.blocks_per_sm;
+    if (k == "baby_l2_mb") return g.baby_l2_mb;
     return fail(EIS_EINVAL, "unknown option '%s'", key);
 }
 

@@ -615,7 +615,8 @@ inline int bsgs_grow(T *&p, size_t &cap, size_t n) {
 
 // max survivors of a segment of `len` candidates (upper bound: all of them)
 inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
-                       BsgsScratch &scr, u32 *qctr, cudaStream_t s, int *launches) {
+                       int baby_l2_mb, BsgsScratch &scr, u32 *qctr, cudaStream_t s,
+                       int *launches) {
     BsgsArgs B;
     B.alpha = alpha_x16 / 16.0f;
     B.ns_log2 = bsgs_ns_log2(d_hi, B.alpha);
@@ -641,11 +642,12 @@ inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, in
     if (cudaMemsetAsync(qctr, 0, 2 * sizeof(u32), s) != cudaSuccess) return -4;
 
     // Baby kernel: the stores being filled are written at random slots; keep
-    // the resident ones within L2 (~80 MB of 126 MB) so partially written
-    // sectors never go to DRAM (measured: 2x DRAM read-modify-write otherwise).
+    // the resident ones within an L2 budget (option "baby_l2_mb") so partially
+    // written sectors are not evicted to DRAM (measured: 2x DRAM
+    // read-modify-write traffic otherwise).
     const size_t store_bytes = (size_t)4 << B.ns_log2;
     int bt = 256;
-    while (bt > 32 && (size_t)num_sms * bt * store_bytes > ((size_t)80 << 20)) bt >>= 1;
+    while (bt > 32 && (size_t)num_sms * bt * store_bytes > ((size_t)baby_l2_mb << 20)) bt >>= 1;
     const size_t smem = (size_t)(2 * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * bt * 4;
     if (cudaFuncSetAttribute(bsgs_baby_kernel<BSGS_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
