@@ -646,13 +646,20 @@ inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, in
     // written sectors are not evicted to DRAM (measured: 2x DRAM
     // read-modify-write traffic otherwise).
     const size_t store_bytes = (size_t)4 << B.ns_log2;
-    int bt = 256;
-    while (bt > 32 && (size_t)num_sms * bt * store_bytes > ((size_t)baby_l2_mb << 20)) bt >>= 1;
+    const int bt = BSGS_THREADS;
     const size_t smem = (size_t)(2 * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * bt * 4;
     if (cudaFuncSetAttribute(bsgs_baby_kernel<BSGS_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return -4;
-    bsgs_baby_kernel<BSGS_KB><<<(unsigned)num_sms, bt, smem, s>>>(a, B, o);
+    int per_sm_b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, bsgs_baby_kernel<BSGS_KB>, bt,
+                                                      smem) != cudaSuccess ||
+        per_sm_b < 1)
+        return -4;
+    const size_t lanes_l2 = ((size_t)baby_l2_mb << 20) / store_bytes;
+    const unsigned bblocks = (unsigned)std::max<size_t>(
+        1, std::min<size_t>((size_t)num_sms * per_sm_b, lanes_l2 / bt));
+    bsgs_baby_kernel<BSGS_KB><<<bblocks, bt, smem, s>>>(a, B, o);
     (*launches)++;
     if (cudaGetLastError() != cudaSuccess) return -4;
     int per_sm_g = 0;
