@@ -156,7 +156,7 @@ typedef struct {
     uint64_t sym_exits;      /* d finished by the symmetry exit */
     uint64_t fallbacks;      /* d re-walked by the half-walk after a BSGS bail-out */
     uint64_t kernel_launches;/* kernels launched by the last call */
-    double walk_ms;          /* device time of the walk kernels (CUDA events) */
+    double walk_ms;          /* device time of the segment loop: sieve + walk kernels (CUDA events) */
     double total_ms;         /* device time of the whole call */
 } eis_stats;
 

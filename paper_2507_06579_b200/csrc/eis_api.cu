@@ -24,15 +24,25 @@
 
 namespace {
 
+// One of two segment buffers: consecutive segments alternate, so the giant
+// kernel of segment i (aux stream) overlaps the sieve and baby kernel of
+// segment i+1 (main stream); events order the reuse of a buffer.
+struct SegBuf {
+    u32 *list = nullptr;
+    size_t list_cap = 0;
+    u32 *ctr = nullptr;              // [0] survivors, [1] work, [2..3] BSGS queue counters
+    BsgsScratch bsgs;
+    cudaEvent_t baby_done = nullptr, giant_done = nullptr;
+};
+
 struct Ctx {
     bool inited = false;
     int device = -1;
     int num_sms = 0;
     std::vector<u32> h_primes;       // odd primes p <= isqrt(EIS_MAX_D)
     u32 *d_primes = nullptr;
-    u32 *d_list = nullptr;
-    size_t list_cap = 0;
-    u32 *d_ctr = nullptr;            // [0] survivor count, [1] work counter, [2] err, [3] work2
+    SegBuf buf[2];
+    u32 *d_err = nullptr;            // in-kernel invariant violations of the current call
     u8 *d_flags = nullptr;
     size_t flags_cap = 0;
     u64 *d_x = nullptr;
@@ -40,8 +50,8 @@ struct Ctx {
     u64 *d_buckets = nullptr;
     size_t buckets_cap = 0;
     u64 *d_stats = nullptr;
-    BsgsScratch bsgs;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;      // giant kernels
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // options
     int mode = EIS_MODE_AUTO;
@@ -128,9 +138,15 @@ int do_init(int device) {
     CUDA_TRY(cudaMalloc(&g.d_primes, g.h_primes.size() * sizeof(u32)));
     CUDA_TRY(cudaMemcpy(g.d_primes, g.h_primes.data(), g.h_primes.size() * sizeof(u32),
                         cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMalloc(&g.d_ctr, 16 * sizeof(u32)));
+    for (auto &b : g.buf) {
+        CUDA_TRY(cudaMalloc(&b.ctr, 8 * sizeof(u32)));
+        CUDA_TRY(cudaEventCreateWithFlags(&b.baby_done, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&b.giant_done, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaMalloc(&g.d_err, sizeof(u32)));
     CUDA_TRY(cudaMalloc(&g.d_stats, ST_NSLOTS * sizeof(u64)));
     CUDA_TRY(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.aux, cudaStreamNonBlocking));
     for (auto &ev : g.ev) CUDA_TRY(cudaEventCreate(&ev));
     CUDA_TRY(cudaFuncSetAttribute(sieve_compact_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -172,16 +188,20 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
               int n, u64 *buckets_dev, cudaStream_t s) {
     const u64 SEG = 1ull << g.segment_log2;
     const int n_small = primes_small();
-    // BSGS keeps one store per survivor of the segment: cap the segment so the
-    // stores stay within ~16 GB of HBM.
+    // BSGS keeps one store per survivor of the segment (two segment buffers):
+    // cap the segment so the stores stay within ~12 GB of HBM per buffer.
     const bool bsgs = want_bsgs(cand_d(i_first));
     u64 seg_cap = SEG;
     if (bsgs) {
         const int nsl = bsgs_ns_log2(cand_d(i_last), g.alpha_x16 / 16.0f);
         const u64 per = ((u64)4 << nsl) + ((u64)4 << nsl) / 2 + sizeof(GiantRec) + 4;
-        seg_cap = std::min<u64>(SEG, std::max<u64>((16ull << 30) / per, 1ull << 16));
+        seg_cap = std::min<u64>(SEG, std::max<u64>((12ull << 30) / per, 1ull << 16));
     }
-    for (u64 seg = i_first; seg <= i_last;) {
+    CUDA_TRY(cudaEventRecord(g.ev[2], s));
+    int iseg = 0;
+    bool used_aux = false;
+    for (u64 seg = i_first; seg <= i_last; iseg++) {
+        SegBuf &bf = g.buf[iseg & 1];
         u64 len = std::min(seg_cap, i_last - seg + 1);
         int b_lo = 0, nb = 0;
         if (x_host) {
@@ -205,22 +225,26 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         }
         const u64 d_last = cand_d(seg + len - 1);
         const int n_primes = primes_upto_sq(d_last);
-        if (ensure(g.d_list, g.list_cap, (size_t)len)) return EIS_ENOMEM;
-        CUDA_TRY(cudaMemsetAsync(g.d_ctr, 0, 16 * sizeof(u32), s));
+        // the buffer is free once the giant kernel that last used it is done
+        if (bsgs) CUDA_TRY(cudaStreamWaitEvent(s, bf.giant_done, 0));
+        if (bf.list_cap < (size_t)len) {
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (ensure(bf.list, bf.list_cap, (size_t)len)) return EIS_ENOMEM;
+        }
+        CUDA_TRY(cudaMemsetAsync(bf.ctr, 0, 8 * sizeof(u32), s));
         const unsigned sblocks = (unsigned)((len + SIEVE_CHUNK - 1) / SIEVE_CHUNK);
         u8 *fseg = flags_dev ? flags_dev + (seg - i_first) : nullptr;
         sieve_compact_kernel<<<sblocks, SIEVE_THREADS, SIEVE_WORDS * sizeof(u32), s>>>(
-            seg, len, g.d_primes, std::min(n_small, n_primes), n_primes, g.d_list, g.d_ctr,
-            fseg);
+            seg, len, g.d_primes, std::min(n_small, n_primes), n_primes, bf.list, bf.ctr, fseg);
         CUDA_TRY(cudaGetLastError());
         g.launches++;
 
         WalkArgs a;
         a.i0 = seg;
-        a.list = g.d_list;
-        a.count = g.d_ctr;
-        a.work = g.d_ctr + 1;
-        a.err = g.d_ctr + 2;
+        a.list = bf.list;
+        a.count = bf.ctr;
+        a.work = bf.ctr + 1;
+        a.err = g.d_err;
         a.flags = fseg;
         a.ckpt = x_host ? x_dev : nullptr;
         a.b_lo = b_lo;
@@ -228,30 +252,48 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.n_ckpt = n;
         a.buckets = buckets_dev;
         a.stats = g.d_stats;
-        CUDA_TRY(cudaEventRecord(g.ev[2], s));
         if (bsgs) {
-            int rc = launch_bsgs(a, len, d_last, g.num_sms, g.alpha_x16, g.baby_l2_mb, g.bsgs,
-                                 g.d_ctr + 3, s, &g.launches);
+            BsgsPlan pl;
+            if (bf.bsgs.tables_bytes < ((size_t)(len + 32) << bsgs_ns_log2(d_last, g.alpha_x16 / 16.0f)))
+                CUDA_TRY(cudaDeviceSynchronize());          // (re)allocation below
+            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.baby_l2_mb, bf.bsgs,
+                                  bf.ctr + 2);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
-                              : fail(EIS_EDEVICE, "BSGS launch failed: %s",
+                              : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
+            if (bsgs_launch_baby(a, pl, s))
+                return fail(EIS_EDEVICE, "BSGS baby launch failed: %s",
+                            cudaGetErrorString(cudaGetLastError()));
+            g.launches++;
+            CUDA_TRY(cudaEventRecord(bf.baby_done, s));
+            CUDA_TRY(cudaStreamWaitEvent(g.aux, bf.baby_done, 0));
+            if (bsgs_launch_giant(a, pl, g.aux))
+                return fail(EIS_EDEVICE, "BSGS giant launch failed: %s",
+                            cudaGetErrorString(cudaGetLastError()));
+            g.launches++;
+            CUDA_TRY(cudaEventRecord(bf.giant_done, g.aux));
+            used_aux = true;
         } else {
             const unsigned wblocks = (unsigned)(g.num_sms * g.blocks_per_sm);
             walk_half_kernel<36><<<wblocks, 256, 0, s>>>(a);
             CUDA_TRY(cudaGetLastError());
             g.launches++;
         }
-        CUDA_TRY(cudaEventRecord(g.ev[3], s));
-        CUDA_TRY(cudaEventSynchronize(g.ev[3]));
-        float ms = 0;
-        cudaEventElapsedTime(&ms, g.ev[2], g.ev[3]);
-        g.walk_ms_acc += ms;
-        u32 err = 0;
-        CUDA_TRY(cudaMemcpy(&err, g.d_ctr + 2, sizeof(u32), cudaMemcpyDeviceToHost));
-        if (err) return fail(EIS_EINTERNAL, "%u in-kernel invariant violations in segment at d=%llu",
-                             err, (unsigned long long)cand_d(seg));
         seg += len;
     }
+    if (used_aux) {                                   // join the aux stream back into s
+        CUDA_TRY(cudaEventRecord(g.ev[3], g.aux));
+        CUDA_TRY(cudaStreamWaitEvent(s, g.ev[3], 0));
+    }
+    CUDA_TRY(cudaEventRecord(g.ev[3], s));
+    CUDA_TRY(cudaEventSynchronize(g.ev[3]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g.ev[2], g.ev[3]);
+    g.walk_ms_acc += ms;
+    u32 err = 0;
+    CUDA_TRY(cudaMemcpy(&err, g.d_err, sizeof(u32), cudaMemcpyDeviceToHost));
+    if (err) return fail(EIS_EINTERNAL, "%u in-kernel invariant violations in [%llu, %llu]", err,
+                         (unsigned long long)cand_d(i_first), (unsigned long long)cand_d(i_last));
     return 0;
 }
 
@@ -284,6 +326,7 @@ int begin_call(cudaStream_t s) {
     g.walk_ms_acc = 0;
     g.launches = 0;
     CUDA_TRY(cudaMemsetAsync(g.d_stats, 0, ST_NSLOTS * sizeof(u64), s));
+    CUDA_TRY(cudaMemsetAsync(g.d_err, 0, sizeof(u32), s));
     CUDA_TRY(cudaEventRecord(g.ev[0], s));
     return 0;
 }
@@ -339,15 +382,21 @@ int eis_init(int device) { return do_init(device); }
 void eis_finalize(void) {
     if (!g.inited) return;
     cudaFree(g.d_primes);
-    cudaFree(g.d_list);
-    cudaFree(g.d_ctr);
+    for (auto &b : g.buf) {
+        cudaFree(b.list);
+        cudaFree(b.ctr);
+        bsgs_free(b.bsgs);
+        if (b.baby_done) cudaEventDestroy(b.baby_done);
+        if (b.giant_done) cudaEventDestroy(b.giant_done);
+    }
+    cudaFree(g.d_err);
     cudaFree(g.d_flags);
     cudaFree(g.d_x);
     cudaFree(g.d_buckets);
     cudaFree(g.d_stats);
-    bsgs_free(g.bsgs);
     for (auto &ev : g.ev) if (ev) cudaEventDestroy(ev);
     if (g.stream) cudaStreamDestroy(g.stream);
+    if (g.aux) cudaStreamDestroy(g.aux);
     Ctx fresh;
     fresh.mode = g.mode;
     fresh.crossover = g.crossover;

@@ -613,11 +613,19 @@ inline int bsgs_grow(T *&p, size_t &cap, size_t n) {
     return 0;
 }
 
-// max survivors of a segment of `len` candidates (upper bound: all of them)
-inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
-                       int baby_l2_mb, BsgsScratch &scr, u32 *qctr, cudaStream_t s,
-                       int *launches) {
+// Per-segment BSGS launch plan: arguments shared by the two kernels.
+struct BsgsPlan {
     BsgsArgs B;
+    BsgsOut o;
+    size_t baby_smem;
+    unsigned baby_blocks, giant_blocks;
+};
+
+// Size the scratch of one segment buffer (`seg_len` candidates bounds its
+// survivors) and choose the launch shapes.  qctr: 2 device counters.
+inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
+                        int baby_l2_mb, BsgsScratch &scr, u32 *qctr) {
+    BsgsArgs &B = pl.B;
     B.alpha = alpha_x16 / 16.0f;
     B.ns_log2 = bsgs_ns_log2(d_hi, B.alpha);
     B.cap = (1 << B.ns_log2) / 2 - 2;
@@ -631,7 +639,7 @@ inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, in
     if (bsgs_grow(scr.lists, scr.lists_n, n * (size_t)lcap)) return -3;
     if (bsgs_grow(scr.recs, scr.recs_n, n)) return -3;
     if (bsgs_grow(scr.queue, scr.queue_n, n)) return -3;
-    BsgsOut o;
+    BsgsOut &o = pl.o;
     o.tables = scr.tables;
     o.lists = scr.lists;
     o.lcap = lcap;
@@ -639,36 +647,41 @@ inline int launch_bsgs(const WalkArgs &a, u64 seg_len, u64 d_hi, int num_sms, in
     o.queue = scr.queue;
     o.qcount = qctr;
     o.qwork = qctr + 1;
-    if (cudaMemsetAsync(qctr, 0, 2 * sizeof(u32), s) != cudaSuccess) return -4;
-
     // Baby kernel: the stores being filled are written at random slots; keep
     // the resident ones within an L2 budget (option "baby_l2_mb") so partially
     // written sectors are not evicted to DRAM (measured: 2x DRAM
     // read-modify-write traffic otherwise).
     const size_t store_bytes = (size_t)4 << B.ns_log2;
     const int bt = BSGS_THREADS;
-    const size_t smem = (size_t)(2 * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * bt * 4;
+    pl.baby_smem = (size_t)(2 * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * bt * 4;
     if (cudaFuncSetAttribute(bsgs_baby_kernel<BSGS_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+                             (int)pl.baby_smem) != cudaSuccess)
         return -4;
     int per_sm_b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, bsgs_baby_kernel<BSGS_KB>, bt,
-                                                      smem) != cudaSuccess ||
+                                                      pl.baby_smem) != cudaSuccess ||
         per_sm_b < 1)
         return -4;
     const size_t lanes_l2 = ((size_t)baby_l2_mb << 20) / store_bytes;
-    const unsigned bblocks = (unsigned)std::max<size_t>(
+    pl.baby_blocks = (unsigned)std::max<size_t>(
         1, std::min<size_t>((size_t)num_sms * per_sm_b, lanes_l2 / bt));
-    bsgs_baby_kernel<BSGS_KB><<<bblocks, bt, smem, s>>>(a, B, o);
-    (*launches)++;
-    if (cudaGetLastError() != cudaSuccess) return -4;
     int per_sm_g = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_g, bsgs_giant_kernel, BSGS_THREADS,
                                                       0) != cudaSuccess ||
         per_sm_g < 1)
         return -4;
-    bsgs_giant_kernel<<<(unsigned)(num_sms * per_sm_g), BSGS_THREADS, 0, s>>>(a, B, o);
-    (*launches)++;
+    pl.giant_blocks = (unsigned)(num_sms * per_sm_g);
+    return 0;
+}
+
+inline int bsgs_launch_baby(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t s) {
+    if (cudaMemsetAsync(pl.o.qcount, 0, 2 * sizeof(u32), s) != cudaSuccess) return -4;
+    bsgs_baby_kernel<BSGS_KB><<<pl.baby_blocks, BSGS_THREADS, pl.baby_smem, s>>>(a, pl.B, pl.o);
+    return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+inline int bsgs_launch_giant(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t s) {
+    bsgs_giant_kernel<<<pl.giant_blocks, BSGS_THREADS, 0, s>>>(a, pl.B, pl.o);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 #endif  // __CUDACC__
