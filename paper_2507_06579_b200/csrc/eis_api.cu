@@ -60,7 +60,7 @@ struct Ctx {
     int segment_log2 = 25;
     int blocks_per_sm = 8;
     int threads = 256;
-    int baby_l2_mb = 40;
+    int baby_l2_mb = 64;
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
