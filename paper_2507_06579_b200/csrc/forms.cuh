@@ -374,8 +374,8 @@ EIS_HD double dexact_div(double n, double dv, double rdv, u32 *err) {
 EIS_HD double dfloor_mod(double a, double b, double rb) {   // b > 0, result in [0, b)
     const double q = floor(a * rb);
     double r = fma(-q, b, a);
-    if (r < 0.0) r += b;
-    else if (r >= b) r -= b;
+    r = r < 0.0 ? r + b : r;                  // selects, not branches
+    r = r >= b ? r - b : r;
     return r;
 }
 

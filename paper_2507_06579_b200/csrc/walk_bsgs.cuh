@@ -102,32 +102,57 @@ EIS_HD void store_insert(Store &S, u32 j, u32 Q, u32 P, u32 t3, float dist2) {
 }
 
 // Look (Q, P) up.  Tables are zero-filled before use (a slot is never 0: j+1 >= 1),
-// so probing stops at the first empty slot.  Split in two so the giant kernel
-// can issue the first probe load, compute the next giant step, and only then
+// so linear probing stops at the first empty slot.  Slots are read four at a
+// time (one aligned 16-byte load per group; at load <= 1/2 the chain almost
+// always ends inside the first group).  Split in two so the giant kernel can
+// issue the first group load, compute the next giant step, and only then
 // resolve the probe (the next step does not depend on the lookup).
 // Returns true with t3 and the stored log2 distance on a hit.
-EIS_HD bool store_resolve(const u32 *tab, const u32 *list, int ns_log2, u32 h, u32 e, u32 Q,
-                          u32 P, u32 &t3, float &dist2) {
+struct Probe {
+    u32 h;              // first slot
+    uint4 grp;          // the aligned group holding slot h
+};
+
+EIS_HD uint4 load_group(const u32 *tab, u32 h) {
+    return *reinterpret_cast<const uint4 *>(tab + (h & ~3u));
+}
+
+EIS_HD Probe store_probe(const u32 *tab, int ns_log2, u32 Q) {
+    Probe p;
+    p.h = store_hash(Q, ns_log2);
+    p.grp = load_group(tab, p.h);
+    return p;
+}
+
+EIS_HD bool store_resolve(const u32 *tab, const u32 *list, int ns_log2, Probe p, u32 Q, u32 P,
+                          u32 &t3, float &dist2) {
     const u32 mask = (1u << ns_log2) - 1;
     const u32 qk = Q >> 2;
+    u32 h = p.h;
+    uint4 g = p.grp;
     for (;;) {
-        if (e == 0) return false;
-        if ((e & 0x3FFFFu) == qk) {
-            const u32 le = list[((e >> 18) & 1023u) - 1];
-            if ((le & 0x7FFFFu) == P) {
-                t3 = e >> 28;
-                dist2 = (float)(le >> 19) * 0.5f;
-                return true;
+        const u32 i0 = h & 3u;
+#pragma unroll
+        for (u32 i = 0; i < 4; i++) {
+            const u32 e = i == 0 ? g.x : (i == 1 ? g.y : (i == 2 ? g.z : g.w));
+            if (i < i0) continue;
+            if (e == 0) return false;
+            if ((e & 0x3FFFFu) == qk) {
+                const u32 le = list[((e >> 18) & 1023u) - 1];
+                if ((le & 0x7FFFFu) == P) {
+                    t3 = e >> 28;
+                    dist2 = (float)(le >> 19) * 0.5f;
+                    return true;
+                }
             }
         }
-        h = (h + 1) & mask;
-        e = tab[h];
+        h = ((h | 3u) + 1) & mask;
+        g = load_group(tab, h);
     }
 }
 EIS_HD bool store_lookup(const u32 *tab, const u32 *list, int ns_log2, u32 Q, u32 P, u32 &t3,
                          float &dist2) {
-    const u32 h = store_hash(Q, ns_log2);
-    return store_resolve(tab, list, ns_log2, h, tab[h], Q, P, t3, dist2);
+    return store_resolve(tab, list, ns_log2, store_probe(tab, ns_log2, Q), Q, P, t3, dist2);
 }
 
 EIS_HD u32 mod3(u32 v) { return v % 3u; }
@@ -282,15 +307,29 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err) {
     float dist = g.dist1 + g.distc - c.lg;
     i64 Q = c.Q, P = c.P;                        // P canonical in (s - Q, s]
     u32 nred = 0;
-    while (Q - P > s) {                          // not reduced (R18): apply rho
-        const i64 q = floor_div(P + s, Q);          // floor((P + sqrt d)/Q)
-        const i64 Pn = q * Q - P;
-        const i64 Qn = exact_div(d - Pn * Pn, Q, err);
-        t = mod3(t + 1u + (u32)((Pn >> 1) & 1));
-        dist += log2_approx((float)fabs((double)Pn + g.sqrtd)) - log2_approx((float)Q);
-        Q = iabs64(Qn);
-        P = s - floor_mod(s - Pn, Q);               // canonical P in (s - Q, s]
-        if (++nred > 4096) { *err += 1; break; }
+    if (Q - P > s) {                             // not reduced (R18): apply rho
+        // exact fp64 integers (|P|, Q < 2^32); Q' = (d - P'^2)/Q with d - P'^2 in int64
+        const double sd = (double)s;
+        double Qd = (double)Q, Pd = (double)P, rQ = rcp64(Qd);
+        do {
+            const double num = Pd + sd;
+            double q = floor(num * rQ);              // floor((P + sqrt d)/Q)
+            const double rr = fma(-q, Qd, num);
+            q = rr < 0.0 ? q - 1.0 : (rr >= Qd ? q + 1.0 : q);
+            const double Pn = fma(q, Qd, -Pd);
+            const i64 Pni = (i64)Pn;
+            const i64 nQ = d - Pni * Pni;
+            const double Qn = rint((double)nQ * rQ);
+            if ((i64)Qn * (i64)Qd != nQ) *err += 1;
+            t = mod3(t + 1u + (u32)((Pni >> 1) & 1));
+            dist += log2_approx((float)fabs(Pn + g.sqrtd)) - log2_approx((float)Qd);
+            Qd = fabs(Qn);
+            rQ = rcp64(Qd);
+            Pd = sd - dfloor_mod(sd - Pn, Qd, rQ);   // canonical P in (s - Q, s]
+            if (++nred > 4096) { *err += 1; break; }
+        } while (Qd - Pd > sd);
+        Q = (i64)Qd;
+        P = (i64)Pd;
     }
     gi.nred = nred;
     g.k++;
@@ -329,10 +368,54 @@ EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u32 *tab, const u32 *list, const
 
 // ------------------------------------------------------------------ kernels --
 // per-d record handed from the baby kernel to the giant kernel (one sector)
-struct __align__(32) GiantRec {
-    u32 off, Q1, P1, Qc, Pc, tk;   // tk = t1 | tc << 2 | k << 4
+// Everything the giant kernel needs to resume a d, precomputed by the baby
+// kernel so a refill is two 32-byte loads (no per-d square roots or divisions
+// in the divergent refill path).
+struct __align__(64) GiantRec {
+    double sqrtd;
+    i64 w1;                        // mu_1's form coefficient (P1^2 - d)/(2 Q1)
+    u32 off, Q1, P1, Qc;           // P1 normalised mod Q1
+    u32 Pc, tk, s, Lk;             // tk = t1 | tc << 2 | k << 4; Lk = L | kcap << 16
     float dist1, distc;
+    u32 pad[2];
 };
+
+EIS_HD GiantRec giant_pack(const GiantLane &g, u32 off) {
+    GiantRec r;
+    r.sqrtd = g.sqrtd;
+    r.w1 = g.m1.w;
+    r.off = off;
+    r.Q1 = (u32)g.m1.Q;
+    r.P1 = (u32)g.m1.P;
+    r.Qc = g.Qc;
+    r.Pc = g.Pc;
+    r.tk = g.t1 | (g.tc << 2) | ((u32)g.k << 4);
+    r.s = (u32)g.s;
+    r.Lk = (u32)g.L | ((u32)g.kcap << 16);
+    r.dist1 = g.dist1;
+    r.distc = g.distc;
+    r.pad[0] = r.pad[1] = 0;
+    return r;
+}
+
+EIS_HD void giant_unpack(GiantLane &g, const GiantRec &r, u64 d) {
+    g.d = d;
+    g.s = (i64)r.s;
+    g.L = (i64)(r.Lk & 0xFFFFu);
+    g.kcap = (int)(r.Lk >> 16);
+    g.sqrtd = r.sqrtd;
+    g.m1.Q = (i64)r.Q1;
+    g.m1.P = (i64)r.P1;
+    g.m1.w = r.w1;
+    g.t1 = r.tk & 3u;
+    g.tc = (r.tk >> 2) & 3u;
+    g.k = (int)(r.tk >> 4);
+    g.dist1 = r.dist1;
+    g.Qc = r.Qc;
+    g.Pc = r.Pc;
+    g.distc = r.distc;
+    g.phase = PH_GIANT;
+}
 
 struct BsgsOut {
     u32 *tables;        // [segment survivors][ns] store slots
@@ -453,15 +536,7 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             const GiantInfo gi = giant_advance(g, B, &err);
             giant++;
             red += gi.nred;
-            GiantRec r;
-            r.off = off;
-            r.Q1 = ln.Q1;
-            r.P1 = ln.P1;
-            r.Qc = g.Qc;
-            r.Pc = g.Pc;
-            r.tk = g.t1 | (g.tc << 2) | ((u32)g.k << 4);
-            r.dist1 = g.dist1;
-            r.distc = g.distc;
+            const GiantRec r = giant_pack(g, off);
             o.recs[idx] = r;
             push = true;
         }
@@ -507,12 +582,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                     const u32 idx = __ldg(o.queue + qi);
                     const GiantRec r = o.recs[idx];
                     off = r.off;
-                    giant_init(g, B, cand_d(a.i0 + off), r.Q1, r.P1, r.tk & 3u, r.dist1, &err);
-                    g.Qc = r.Qc;
-                    g.Pc = r.Pc;
-                    g.tc = (r.tk >> 2) & 3u;
-                    g.k = (int)(r.tk >> 4);
-                    g.distc = r.distc;
+                    giant_unpack(g, r, cand_d(a.i0 + off));
                     pending = true;               // mu'_2 is probed with the next advance
                     tab = o.tables + ((u64)idx << B.ns_log2);
                     list = o.lists + (u64)idx * o.lcap;
@@ -527,17 +597,16 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             // for k = 2: `pending` false) while computing mu'_{k+1}
             const u32 pQ = g.Qc, pP = g.Pc, pt = g.tc;
             const float pdist = g.distc;
-            u32 h = 0, e0 = 0;
-            if (pending) {
-                h = store_hash(pQ, B.ns_log2);
-                e0 = tab[h];
-            }
+            Probe pr;
+            pr.h = 0;
+            pr.grp = make_uint4(0, 0, 0, 0);
+            if (pending) pr = store_probe(tab, B.ns_log2, pQ);
             const GiantInfo gi = giant_advance(g, B, &err);
             giant++;
             red += gi.nred;
             u32 te;
             float de;
-            if (pending && store_resolve(tab, list, B.ns_log2, h, e0, pQ, pP, te, de) &&
+            if (pending && store_resolve(tab, list, B.ns_log2, pr, pQ, pP, te, de) &&
                 giant_hit(te, de, pt, pdist, g.res)) {
                 g.phase = PH_DONE;
             } else if (g.k > g.kcap) {
