@@ -61,6 +61,7 @@ struct Ctx {
     int blocks_per_sm = 8;
     int threads = 256;
     int baby_l2_mb = 64;
+    int giant_ctas = 0;
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
@@ -256,8 +257,8 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
             BsgsPlan pl;
             if (bf.bsgs.tables_bytes < ((size_t)(len + 32) << bsgs_ns_log2(d_last, g.alpha_x16 / 16.0f)))
                 CUDA_TRY(cudaDeviceSynchronize());          // (re)allocation below
-            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.baby_l2_mb, bf.bsgs,
-                                  bf.ctr + 2);
+            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.baby_l2_mb,
+                                  g.giant_ctas, bf.bsgs, bf.ctr + 2);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -404,6 +405,7 @@ void eis_finalize(void) {
     fresh.segment_log2 = g.segment_log2;
     fresh.blocks_per_sm = g.blocks_per_sm;
     fresh.baby_l2_mb = g.baby_l2_mb;
+    fresh.giant_ctas = g.giant_ctas;
     g = fresh;
 }
 
@@ -427,6 +429,9 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "baby_l2_mb") {
         if (v < 1 || v > 4096) return fail(EIS_EINVAL, "baby_l2_mb must be in [1, 4096]");
         g.baby_l2_mb = (int)v;
+    } else if (k == "giant_ctas") {
+        if (v < 0 || v > 32) return fail(EIS_EINVAL, "giant_ctas must be in [0, 32]");
+        g.giant_ctas = (int)v;
     } else if (k == "blocks_per_sm") {
         if (v < 1 || v > 32) return fail(EIS_EINVAL, "blocks_per_sm must be in [1, 32]");
         g.blocks_per_sm = (int)v;
@@ -445,6 +450,7 @@ int64_t eis_get_option(const char *key) {
     if (k == "segment_log2") return g.segment_log2;
     if (k == "blocks_per_sm") return g.blocks_per_sm;
     if (k == "baby_l2_mb") return g.baby_l2_mb;
+    if (k == "giant_ctas") return g.giant_ctas;
     return fail(EIS_EINVAL, "unknown option '%s'", key);
 }
 

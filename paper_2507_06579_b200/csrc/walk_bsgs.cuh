@@ -693,7 +693,7 @@ struct BsgsPlan {
 // Size the scratch of one segment buffer (`seg_len` candidates bounds its
 // survivors) and choose the launch shapes.  qctr: 2 device counters.
 inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
-                        int baby_l2_mb, BsgsScratch &scr, u32 *qctr) {
+                        int baby_l2_mb, int giant_ctas, BsgsScratch &scr, u32 *qctr) {
     BsgsArgs &B = pl.B;
     B.alpha = alpha_x16 / 16.0f;
     B.ns_log2 = bsgs_ns_log2(d_hi, B.alpha);
@@ -739,7 +739,9 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
                                                       0) != cudaSuccess ||
         per_sm_g < 1)
         return -4;
-    pl.giant_blocks = (unsigned)(num_sms * per_sm_g);
+    // giant_ctas > 0 caps the giant kernel's CTAs per SM so that the next
+    // segment's baby kernel (other stream) can be resident at the same time
+    pl.giant_blocks = (unsigned)(num_sms * (giant_ctas > 0 ? std::min(giant_ctas, per_sm_g) : per_sm_g));
     return 0;
 }
 
