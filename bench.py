@@ -35,8 +35,8 @@ METRIC = "squarefree d≡5 mod 8 classified/sec (whole box) at d≈10^10; 1/2/4/
 UNIT = "d/s"
 SM_MAX_MHZ_FALLBACK = 1965.0
 # Algorithmic thread-operations per unit of work:
-OPS_PER_BABY = 19      # one rho step + residue + symmetry tests (K3)
-OPS_PER_GIANT = 0      # replaced once BSGS lands (K3-giant)
+OPS_PER_BABY = 20      # SASS of one rho step + residue + exit tests (K3 HALF)
+OPS_PER_GIANT = 700    # measured thread-instructions per giant step (K3 BSGS)
 
 
 def _env_int(k, d):

@@ -14,7 +14,7 @@
  * as its class in (O_K/2O_K)^* = F_4^* = Z/3 (l.601-603), with continued-
  * fraction baby steps rho (l.541), and NUCOMP/NUDUPL giant steps (l.617-756).
  *
- * Residue labelling (one fixed choice, reading R3): an element
+ * Residue labelling (one fixed choice, reading R30): an element
  * a*1 + b*w of O_K, w = (1+sqrt d)/2, with (a mod 2, b mod 2) = (1,0), (0,1),
  * (1,1) has residue t = 0, 1, 2.  d in E  <=>  t(eps_d) = 0.
  *

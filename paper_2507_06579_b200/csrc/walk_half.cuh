@@ -8,9 +8,9 @@
 //   theta_{j+2} = ((P_{j+1} + sqrt d)/Q_j) theta_{j+1},
 // carrying theta only as its residue t in Z/3.  Since
 // Q_j = 2 mod 4 and P_{j+1} is odd, (P_{j+1} + sqrt d)/Q_j = ((P-1)/2 + w)/(Q_j/2)
-// has residue 1 if P_{j+1} = 1 mod 4 and 2 if P_{j+1} = 3 mod 4 (R5).
+// has residue 1 if P_{j+1} = 1 mod 4 and 2 if P_{j+1} = 3 mod 4 (R31).
 // The walk stops at the symmetry point of Algorithm 1 (PAPER.md l.553-556,
-// "if Q_j = Q_{j-1} or P_j = P_{j-1}"), where (R7)
+// "if Q_j = Q_{j-1} or P_j = P_{j-1}"), where (R13)
 //   Q_j = Q_{j-1}:          t(eps) = t(theta_j) + t(theta_{j+1}),
 //   P_j = P_{j-1}, j >= 2:  t(eps) = 2 t(theta_j).
 //
@@ -75,7 +75,7 @@ EIS_HD bool baby_step(BabyState &st) {
 }
 
 // t(eps) (not reduced mod 3) at the symmetry point reached by baby_step
-// (R7):
+// (R13):
 //   Q_j = Q_{j-1}:  t(theta_j) + t(theta_{j+1});   P_j = P_{j-1}:  2 t(theta_j).
 EIS_HD u32 baby_result(const BabyState &st) {
     const u32 inc = (st.P & 2u) + 2u;        // 2 (t(theta_{j+1}) - t(theta_j))

@@ -1,0 +1,102 @@
+"""Multi-GPU host logic on CPU: sharding and the one all-reduce, world_size 2 (gloo).
+
+The path shards with no data exchange; the only collective is
+the all-reduce of the 2n checkpoint buckets.  Here each rank fills the buckets
+of its shard with the ORACLE (test infrastructure standing in for the CUDA
+kernels, which need a GPU); the product functions under test are
+``shard_bounds`` and ``allreduce_buckets``.  The combined counts must equal a
+single-process count for any world size.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import c_oracle
+from paper_2507_06579_b200.dist import allreduce_buckets, shard_bounds
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_buckets(a: int, b: int, x: np.ndarray) -> torch.Tensor:
+    """Bucket counts of d in (a, b] (bucket(d) = least i with d <= x[i]) by the oracle."""
+    n = len(x)
+    out = np.zeros(2 * n, dtype=np.int64)
+    top = min(b, int(x[-1]))
+    if top > a:
+        f = c_oracle.classify_range(a + 1, top)
+        first = (a + 1) + (5 - (a + 1)) % 8
+        d = first + 8 * np.arange(f.size, dtype=np.int64)
+        bidx = np.searchsorted(x.astype(np.int64), d, side="left")
+        np.add.at(out, bidx[f != c_oracle.NOT_IN_D], 1)
+        np.add.at(out, n + bidx[f == 0], 1)
+    return torch.from_numpy(out)
+
+
+def _worker(rank, world, port, lo, x, balance, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = np.asarray(x, dtype=np.uint64)
+        a, b = shard_bounds(lo, int(x[-1]), world, rank, balance)
+        buckets = oracle_buckets(a, b, x)
+        allreduce_buckets(buckets)
+        q.put((rank, (a, b), buckets.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,balance", [(2, "flat"), (2, "prefix"), (3, "prefix")])
+def test_sharded_allreduce_matches_single_process(world, balance):
+    lo = 0 if balance == "prefix" else 123_457
+    x = np.array([200_000, 350_001, 500_000, 777_777], dtype=np.uint64)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, lo, x, balance, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    shards = [r[1] for r in res]
+    # shards are contiguous, disjoint and cover (lo, x[-1]]
+    assert shards[0][0] == lo and shards[-1][1] == int(x[-1])
+    for (a0, b0), (a1, b1) in zip(shards, shards[1:]):
+        assert b0 == a1 and a0 <= b0 and b0 % 8 == 0
+    # every rank holds the same reduced buckets, equal to the single-process ones
+    want = oracle_buckets(lo, int(x[-1]), x).numpy()
+    for _, _, got in res:
+        assert np.array_equal(np.asarray(got), want)
+    # prefix of the reduced buckets = counting functions
+    n = len(x)
+    cD, cE = c_oracle.count_window(lo, x)
+    assert np.array_equal(np.cumsum(want[:n]), cD.astype(np.int64))
+    assert np.array_equal(np.cumsum(want[n:]), cE.astype(np.int64))
+
+
+def test_shard_bounds_properties():
+    for world in (1, 2, 4, 8):
+        for balance in ("flat", "prefix"):
+            lo, hi = 9 * 10**9, 10**10
+            cuts = [shard_bounds(lo, hi, world, r, balance) for r in range(world)]
+            assert cuts[0][0] == lo and cuts[-1][1] == hi
+            for (a0, b0), (a1, b1) in zip(cuts, cuts[1:]):
+                assert b0 == a1 and b0 % 8 == 0
+    # prefix balancing gives later (costlier per d) shards less width
+    c = [shard_bounds(0, 10**9, 4, r, "prefix") for r in range(4)]
+    widths = [b - a for a, b in c]
+    assert widths == sorted(widths, reverse=True)
