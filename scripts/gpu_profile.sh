@@ -7,4 +7,3 @@ echo "launch list exit $?"
 $CMD > gpurun_out/prof_plain2.json 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:walk -s 1 -c 1 -o gpurun_out/prof_walk $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full exit $?"
-ls -la gpurun_out
