@@ -51,6 +51,15 @@ EIS_HD u32 f2u_bits(float f) {
 #endif
 }
 
+// clamp to [0, 1] (FADD.SAT / FMUL.SAT modifier on the device)
+EIS_HD float sat01(float x) {
+#ifdef __CUDA_ARCH__
+    return __saturatef(x);
+#else
+    return fminf(fmaxf(x, 0.f), 1.f);
+#endif
+}
+
 // index of the lowest set bit (x != 0)
 EIS_HD int __builtin_ctz_portable(u32 x) {
 #ifdef __CUDA_ARCH__

@@ -83,6 +83,53 @@ EIS_HD u32 baby_result(const BabyState &st) {
     return (st.Q == st.Qp) ? (st.t2 + t2b) >> 1 : t2b;
 }
 
+// ---- the same step in exact FP32 integer arithmetic (the half-walk kernel's
+// form).  Every value is an integer < 2^24, so FADD/FFMA are exact:
+//   q0 = round(num * rcp(Q)) (FFMA with the 2^23 magic), r0 = num - q0 Q exact
+//   in [-Q, Q); c = sat(-r0) is 1 iff r0 < 0; q = q0 - c, r = r0 + c Q;
+//   P_j = s - r;  Q_j = fma(q, P_{j-1} - P_j, Q_{j-2}) is exact because the true
+//   q (P_{j-1} - P_j) = Q_j - Q_{j-2} has magnitude < 2^20 and FFMA rounds once.
+// The residue bit of P_j comes from its exact float image + 2^23.  Moving the
+// recurrence off the integer ALU pipe (half rate) onto the FP32 pipes balances
+// the step (K3 HALF).
+struct BabyStateF {
+    float s, P, Q, Qp;  // isqrt(d), P_j, Q_j, Q_{j-1}
+    u32 t2;             // 2 t(theta_{j+1}) (not reduced mod 3)
+};
+
+EIS_HD BabyStateF baby_to_f(const BabyState &b) {
+    BabyStateF f;
+    f.s = (float)b.s;
+    f.P = (float)b.P;
+    f.Q = (float)b.Q;
+    f.Qp = (float)b.Qp;
+    f.t2 = b.t2;
+    return f;
+}
+
+EIS_HD bool baby_step_f(BabyStateF &st) {
+    const float num = st.P + st.s;
+    const float rq = rcp_approx(st.Q);
+    const float q0 = fmaf(num, rq, 8388608.0f) - 8388608.0f;   // round(num/Q)
+    const float r0 = fmaf(-q0, st.Q, num);                      // exact, in [-Q, Q)
+    const float c = sat01(-r0);                                 // 1 iff r0 < 0
+    const float q = q0 - c;                                     // floor(num/Q)
+    const float Pn = st.s - fmaf(c, st.Q, r0);                  // P_j = s - (num mod Q)
+    const float Qn = fmaf(q, st.P - Pn, st.Qp);                 // Q_j, exact
+    st.t2 += (f2u_bits(Pn + 8388608.0f) & 2u) + 2u;             // residue of (P_j + sqrt d)/Q_{j-1}
+    const bool eP = (Pn == st.P);
+    st.Qp = st.Q;
+    st.Q = Qn;
+    st.P = Pn;
+    return (Qn == st.Qp) | eP;
+}
+
+EIS_HD u32 baby_result_f(const BabyStateF &st) {
+    const u32 inc = (((u32)st.P) & 2u) + 2u;   // 2 (t(theta_{j+1}) - t(theta_j))
+    const u32 t2b = st.t2 - inc;               // 2 t(theta_j)
+    return (st.Q == st.Qp) ? (st.t2 + t2b) >> 1 : t2b;
+}
+
 template <int KSTEPS>
 __global__ void __launch_bounds__(256)
 walk_half_kernel(WalkArgs a) {
@@ -92,7 +139,8 @@ walk_half_kernel(WalkArgs a) {
 
     const int lane = threadIdx.x & 31;
     const u32 n = *a.count;
-    BabyState st;
+    BabyState st0;
+    BabyStateF st;
     u64 d = 0;
     u32 off = 0;
     bool active = false, exhausted = false;
@@ -124,9 +172,10 @@ walk_half_kernel(WalkArgs a) {
                     off = __ldg(a.list + idx);
                     d = cand_d(a.i0 + off);
                     u32 r1;
-                    if (baby_init(st, d, &r1)) {
+                    if (baby_init(st0, d, &r1)) {
                         finish(r1);            // period closes at j = 1 (d = P_1^2 + 4)
                     } else {
+                        st = baby_to_f(st0);
                         active = true;
                     }
                 } else {
@@ -140,11 +189,11 @@ walk_half_kernel(WalkArgs a) {
             int k = 0;
 #pragma unroll 6
             for (; k < KSTEPS; k++) {
-                if (baby_step(st)) { fin = true; break; }
+                if (baby_step_f(st)) { fin = true; break; }
             }
             steps += (u32)(k + fin);
             if (fin) {
-                finish(baby_result(st));
+                finish(baby_result_f(st));
                 active = false;
             }
         }

@@ -35,9 +35,13 @@ int main(int argc, char **argv) {
             u32 r1;
             baby = 1;
             if (baby_init(st, d, &r1)) res = r1;
-            else {
+            else if (ns_fixed == 99) {                      // integer form of the step
                 for (;;) { baby++; if (baby_step(st)) break; }
                 res = baby_result(st);
+            } else {                                        // FP32 form (the kernel's)
+                BabyStateF sf = baby_to_f(st);
+                for (;;) { baby++; if (baby_step_f(sf)) break; }
+                res = baby_result_f(sf);
             }
         } else {
             B.ns_log2 = ns_fixed ? ns_fixed : bsgs_ns_log2(d, B.alpha);
