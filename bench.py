@@ -35,7 +35,11 @@ METRIC = "squarefree d≡5 mod 8 classified/sec (whole box) at d≈10^10; 1/2/4/
 UNIT = "d/s"
 SM_MAX_MHZ_FALLBACK = 1965.0
 # Algorithmic thread-operations per unit of work:
-OPS_PER_BABY = 20      # SASS of one rho step + residue + exit tests (K3 HALF)
+# Algorithmic ops of one rho step (+ residue + exit tests) in its integer
+# formulation: 20 (fixed reference, DESIGN.md 4 K3 HALF).  The kernel's FP32
+# formulation issues 17 instructions per step (INSTR_PER_BABY) for the same work.
+OPS_PER_BABY = 20
+INSTR_PER_BABY = 17
 OPS_PER_GIANT = 700    # measured thread-instructions per giant step (K3 BSGS)
 
 
@@ -290,12 +294,19 @@ def main():
             "roofline": {
                 "bound": "alu", "kernel": "walk (K3+K4)",
                 "achieved": achieved, "peak": peak, "unit": "Tops/s", "frac": achieved / peak,
-                "traffic": None,
+                "traffic": 50.8e6 if stats["giant_steps"] == 0 else None,
+                "traffic_note": "dram read+write bytes per walk launch, ncu --set full "
+                                "(profiles/r01_half_walk.txt); algorithmic bytes = 4 per d "
+                                "(survivor list) = 50.7 MB",
+                "issue_utilisation": (INSTR_PER_BABY * stats["baby_steps"] + OPS_PER_GIANT
+                                      * stats["giant_steps"]) / (walk_ms_max / 1e3) / 1e12 / peak,
                 "ops_per_launch": ops_per_launch,
                 "walk_ms_per_launch": walk_ms_max,
                 "walk_share_of_step": walk_ms_max / (tot_ms_max / args.steps),
-                "basis": f"{OPS_PER_BABY} ops/baby step, {OPS_PER_GIANT} ops/giant step; peak = "
-                         f"148 SM x 4 SMSP x 32 lanes x {sm_clk:.0f} MHz (DESIGN.md)",
+                "basis": f"{OPS_PER_BABY} algorithmic ops/baby step (integer formulation; the "
+                         f"kernel issues {INSTR_PER_BABY} instructions), {OPS_PER_GIANT} "
+                         f"ops/giant step; peak = 148 SM x 4 SMSP x 32 lanes x {sm_clk:.0f} MHz "
+                         f"issue slots (DESIGN.md 4)",
             },
             "clocks": clocks,
             "stats_per_rank_step": {k: stats[k] for k in ("d_classified", "baby_steps",
