@@ -51,6 +51,17 @@ EIS_HD u32 f2u_bits(float f) {
 #endif
 }
 
+// fma rounded toward zero (FFMA.RZ).  The host emulation computes the exact
+// product-sum in double (a 20-bit x 24-bit product plus 2^23 is exact there)
+// and truncates, which equals RZ to float for results in [2^23, 2^24).
+EIS_HD float fma_rz(float a, float b, float c) {
+#ifdef __CUDA_ARCH__
+    return __fmaf_rz(a, b, c);
+#else
+    return (float)trunc((double)a * (double)b + (double)c);
+#endif
+}
+
 // clamp to [0, 1] (FADD.SAT / FMUL.SAT modifier on the device)
 EIS_HD float sat01(float x) {
 #ifdef __CUDA_ARCH__

@@ -620,8 +620,12 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 if (baby_init(st, g.d, &r1)) {
                     g.res = r1;
                 } else {
-                    do { baby++; } while (!baby_step(st));
-                    g.res = baby_result(st);
+                    const u32 cap = half_step_cap(st.s);
+                    u32 j = 0;
+                    bool ok;
+                    do { baby++; ok = baby_step(st); } while (!ok && ++j <= cap);
+                    if (ok) g.res = baby_result(st);
+                    else { err++; g.res = 0xFFu; }
                 }
                 g.phase = PH_DONE;
             }

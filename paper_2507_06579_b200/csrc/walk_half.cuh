@@ -84,23 +84,29 @@ EIS_HD u32 baby_result(const BabyState &st) {
 }
 
 // ---- the same step in exact FP32 integer arithmetic (the half-walk kernel's
-// form).  Every value is an integer < 2^24, so FADD/FFMA are exact:
-//   q0 = round(num * rcp(Q)) (FFMA with the 2^23 magic), r0 = num - q0 Q exact
-//   in [-Q, Q); c = sat(-r0) is 1 iff r0 < 0; q = q0 - c, r = r0 + c Q;
-//   P_j = s - r;  Q_j = fma(q, P_{j-1} - P_j, Q_{j-2}) is exact because the true
-//   q (P_{j-1} - P_j) = Q_j - Q_{j-2} has magnitude < 2^20 and FFMA rounds once.
-// The residue bit of P_j comes from its exact float image + 2^23.  Moving the
-// recurrence off the integer ALU pipe (half rate) onto the FP32 pipes balances
-// the step (K3 HALF).
+// form).  Every value is an integer < 2^24, so FADD/FFMA on them are exact.
+//  * P is kept as Pm = P + 2^23: the bits of Pm are 0x4B000000 + P, so the
+//    residue bit (P & 2) is one LOP3 and P_j = P_{j-1} is a float compare.
+//  * q = floor(num/Q) exactly, num = P + s < 2^20, by one FFMA rounded toward
+//    zero: num * rqb + 2^23 with rqb = rcp(Q)(1 + 2^-21).  With |rel err of
+//    rcp| <= 2^-22, rqb lies in [1/Q, (1/Q)(1 + 0.82 2^-20)), so num*rqb lies in
+//    [num/Q, num/Q + 0.82/Q) and its floor is floor(num/Q) (the fractional part
+//    of num/Q is at most 1 - 1/Q).  No correction step.
+//  * r = num - q Q, P_j = s - r, Q_j = fma(q, P_{j-1} - P_j, Q_{j-2}); the FFMA
+//    is exact because the true q (P_{j-1} - P_j) = Q_j - Q_{j-2} is < 2^20.
+// 14 SASS instructions per step, 4 of them on the half-rate ALU pipe
+// (K3 HALF).
 struct BabyStateF {
-    float s, P, Q, Qp;  // isqrt(d), P_j, Q_j, Q_{j-1}
+    float sm, sp;       // s - 2^23, s + 2^23
+    float Pm, Q, Qp;    // P_j + 2^23, Q_j, Q_{j-1}
     u32 t2;             // 2 t(theta_{j+1}) (not reduced mod 3)
 };
 
 EIS_HD BabyStateF baby_to_f(const BabyState &b) {
     BabyStateF f;
-    f.s = (float)b.s;
-    f.P = (float)b.P;
+    f.sm = (float)b.s - 8388608.0f;
+    f.sp = (float)b.s + 8388608.0f;
+    f.Pm = (float)b.P + 8388608.0f;
     f.Q = (float)b.Q;
     f.Qp = (float)b.Qp;
     f.t2 = b.t2;
@@ -108,27 +114,31 @@ EIS_HD BabyStateF baby_to_f(const BabyState &b) {
 }
 
 EIS_HD bool baby_step_f(BabyStateF &st) {
-    const float num = st.P + st.s;
-    const float rq = rcp_approx(st.Q);
-    const float q0 = fmaf(num, rq, 8388608.0f) - 8388608.0f;   // round(num/Q)
-    const float r0 = fmaf(-q0, st.Q, num);                      // exact, in [-Q, Q)
-    const float c = sat01(-r0);                                 // 1 iff r0 < 0
-    const float q = q0 - c;                                     // floor(num/Q)
-    const float Pn = st.s - fmaf(c, st.Q, r0);                  // P_j = s - (num mod Q)
-    const float Qn = fmaf(q, st.P - Pn, st.Qp);                 // Q_j, exact
-    st.t2 += (f2u_bits(Pn + 8388608.0f) & 2u) + 2u;             // residue of (P_j + sqrt d)/Q_{j-1}
-    const bool eP = (Pn == st.P);
+    const float num = st.Pm + st.sm;                            // P + s
+    const float rqb = rcp_approx(st.Q) * 1.000000476837158203125f;   // (1 + 2^-21)
+    const float q = fma_rz(num, rqb, 8388608.0f) - 8388608.0f;  // floor(num/Q)
+    const float r = fmaf(-q, st.Q, num);                        // num mod Q, exact
+    const float Pnm = st.sp - r;                                // P_j + 2^23
+    const float Qn = fmaf(q, st.Pm - Pnm, st.Qp);               // Q_j, exact
+    st.t2 += (f2u_bits(Pnm) & 2u) + 2u;                         // residue of (P_j + sqrt d)/Q_{j-1}
+    const bool eP = (Pnm == st.Pm);
     st.Qp = st.Q;
     st.Q = Qn;
-    st.P = Pn;
+    st.Pm = Pnm;
     return (Qn == st.Qp) | eP;
 }
 
 EIS_HD u32 baby_result_f(const BabyStateF &st) {
-    const u32 inc = (((u32)st.P) & 2u) + 2u;   // 2 (t(theta_{j+1}) - t(theta_j))
-    const u32 t2b = st.t2 - inc;               // 2 t(theta_j)
+    const u32 inc = (f2u_bits(st.Pm) & 2u) + 2u;   // 2 (t(theta_{j+1}) - t(theta_j))
+    const u32 t2b = st.t2 - inc;                   // 2 t(theta_j)
     return (st.Q == st.Qp) ? (st.t2 + t2b) >> 1 : t2b;
 }
+
+// Safety cap on rho steps per d: the half period is at most R/ln 2 <= ~20 sqrt(d)
+// (h R < sqrt(d)(ln d + 2)/2 and two rho steps advance the distance by >= ln 2).
+// A walk beyond the cap means a violated arithmetic invariant: it is counted
+// as an error (the call fails with EIS_EINTERNAL) instead of looping forever.
+EIS_HD u32 half_step_cap(u32 s) { return 48u * s + 64u; }
 
 template <int KSTEPS>
 __global__ void __launch_bounds__(256)
@@ -144,7 +154,7 @@ walk_half_kernel(WalkArgs a) {
     u64 d = 0;
     u32 off = 0;
     bool active = false, exhausted = false;
-    u32 n_done = 0, n_sym = 0;
+    u32 n_done = 0, n_sym = 0, n_err = 0, dsteps = 0, cap = 0;
     u64 steps = 0;
     auto finish = [&](u32 res) {
         const u32 t = res % 3;
@@ -176,6 +186,8 @@ walk_half_kernel(WalkArgs a) {
                         finish(r1);            // period closes at j = 1 (d = P_1^2 + 4)
                     } else {
                         st = baby_to_f(st0);
+                        dsteps = 0;
+                        cap = half_step_cap(st0.s);
                         active = true;
                     }
                 } else {
@@ -192,8 +204,13 @@ walk_half_kernel(WalkArgs a) {
                 if (baby_step_f(st)) { fin = true; break; }
             }
             steps += (u32)(k + fin);
+            dsteps += (u32)(k + fin);
             if (fin) {
                 finish(baby_result_f(st));
+                active = false;
+            } else if (dsteps > cap) {
+                n_err++;
+                finish(0xFFu);
                 active = false;
             }
         }
@@ -203,6 +220,8 @@ walk_half_kernel(WalkArgs a) {
     u64 s_steps = warp_sum_u64(steps);
     u64 s_done = warp_sum_u64(n_done);
     u64 s_sym = warp_sum_u64(n_sym);
+    const u32 s_err = __reduce_add_sync(FULL_MASK, n_err);
+    if (lane == 0 && s_err) atomicAdd(a.err, s_err);
     if (lane == 0 && a.stats) {
         atomicAdd((unsigned long long *)&a.stats[ST_BABY], (unsigned long long)s_steps);
         atomicAdd((unsigned long long *)&a.stats[ST_D], (unsigned long long)s_done);
