@@ -35,11 +35,12 @@ METRIC = "squarefree d≡5 mod 8 classified/sec (whole box) at d≈10^10; 1/2/4/
 UNIT = "d/s"
 SM_MAX_MHZ_FALLBACK = 1965.0
 # Algorithmic thread-operations per unit of work:
-# Algorithmic ops of one rho step (+ residue + exit tests) in its integer
-# formulation: 20 (fixed reference, DESIGN.md 4 K3 HALF).  The kernel's FP32
-# formulation issues 17 instructions per step (INSTR_PER_BABY) for the same work.
-OPS_PER_BABY = 20
-INSTR_PER_BABY = 17
+# Work per unit: one rho step (+ residue + exit tests) is 14 SASS
+# instructions in the kernel's FP32 formulation (cuobjdump), so `frac` is the
+# share of the chip's issue slots spent on step instructions.  SURVEY 8(d)'s
+# generic u32 step is 34 instructions; `work_equiv_generic` reports that view.
+OPS_PER_BABY = 14
+GENERIC_PER_BABY = 34
 OPS_PER_GIANT = 700    # measured thread-instructions per giant step (K3 BSGS)
 
 
@@ -298,15 +299,14 @@ def main():
                 "traffic_note": "dram read+write bytes per walk launch, ncu --set full "
                                 "(profiles/r01_half_walk.txt); algorithmic bytes = 4 per d "
                                 "(survivor list) = 50.7 MB",
-                "issue_utilisation": (INSTR_PER_BABY * stats["baby_steps"] + OPS_PER_GIANT
-                                      * stats["giant_steps"]) / (walk_ms_max / 1e3) / 1e12 / peak,
+                "work_equiv_generic": (GENERIC_PER_BABY * stats["baby_steps"] + OPS_PER_GIANT
+                                       * stats["giant_steps"]) / (walk_ms_max / 1e3) / 1e12 / peak,
                 "ops_per_launch": ops_per_launch,
                 "walk_ms_per_launch": walk_ms_max,
                 "walk_share_of_step": walk_ms_max / (tot_ms_max / args.steps),
-                "basis": f"{OPS_PER_BABY} algorithmic ops/baby step (integer formulation; the "
-                         f"kernel issues {INSTR_PER_BABY} instructions), {OPS_PER_GIANT} "
-                         f"ops/giant step; peak = 148 SM x 4 SMSP x 32 lanes x {sm_clk:.0f} MHz "
-                         f"issue slots (DESIGN.md 4)",
+                "basis": f"{OPS_PER_BABY} SASS instructions per rho step, {OPS_PER_GIANT} "
+                         f"thread-instructions per giant step; peak = 148 SM x 4 SMSP x 32 "
+                         f"lanes x {sm_clk:.0f} MHz issue slots (DESIGN.md 4)",
             },
             "clocks": clocks,
             "stats_per_rank_step": {k: stats[k] for k in ("d_classified", "baby_steps",
