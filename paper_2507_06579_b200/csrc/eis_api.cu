@@ -63,6 +63,7 @@ struct Ctx {
     int threads = 256;
     int baby_l2_mb = 64;
     int giant_ctas = 0;
+    int half_ksteps = 36;
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
@@ -277,7 +278,12 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
             used_aux = true;
         } else {
             const unsigned wblocks = (unsigned)(g.num_sms * g.blocks_per_sm);
-            walk_half_kernel<36><<<wblocks, 256, 0, s>>>(a);
+            switch (g.half_ksteps) {
+                case 18: walk_half_kernel<18><<<wblocks, 256, 0, s>>>(a); break;
+                case 72: walk_half_kernel<72><<<wblocks, 256, 0, s>>>(a); break;
+                case 144: walk_half_kernel<144><<<wblocks, 256, 0, s>>>(a); break;
+                default: walk_half_kernel<36><<<wblocks, 256, 0, s>>>(a); break;
+            }
             CUDA_TRY(cudaGetLastError());
             g.launches++;
         }
@@ -407,6 +413,7 @@ void eis_finalize(void) {
     fresh.blocks_per_sm = g.blocks_per_sm;
     fresh.baby_l2_mb = g.baby_l2_mb;
     fresh.giant_ctas = g.giant_ctas;
+    fresh.half_ksteps = g.half_ksteps;
     g = fresh;
 }
 
@@ -433,6 +440,10 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "giant_ctas") {
         if (v < 0 || v > 32) return fail(EIS_EINVAL, "giant_ctas must be in [0, 32]");
         g.giant_ctas = (int)v;
+    } else if (k == "half_ksteps") {
+        if (v != 18 && v != 36 && v != 72 && v != 144)
+            return fail(EIS_EINVAL, "half_ksteps must be 18, 36, 72 or 144");
+        g.half_ksteps = (int)v;
     } else if (k == "blocks_per_sm") {
         if (v < 1 || v > 32) return fail(EIS_EINVAL, "blocks_per_sm must be in [1, 32]");
         g.blocks_per_sm = (int)v;
@@ -452,6 +463,7 @@ int64_t eis_get_option(const char *key) {
     if (k == "blocks_per_sm") return g.blocks_per_sm;
     if (k == "baby_l2_mb") return g.baby_l2_mb;
     if (k == "giant_ctas") return g.giant_ctas;
+    if (k == "half_ksteps") return g.half_ksteps;
     return fail(EIS_EINVAL, "unknown option '%s'", key);
 }
 
