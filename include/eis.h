@@ -97,7 +97,7 @@ EIS_API const char *eis_last_error(void);
  *  "blocks_per_sm" HALF walk kernel CTAs per SM
  *  "baby_l2_mb"    BSGS baby kernel: MB of L2 its resident stores may occupy
  *  "giant_ctas"    BSGS giant kernel CTAs per SM (0 = occupancy maximum)
- *  "half_ksteps"   HALF walk: rho steps per lane between refills (18/36/72/144) */
+ *  "half_ksteps"   HALF walk: rho steps per lane between refills (0 = auto, 18/36/72/144) */
 EIS_API int eis_set_option(const char *key, int64_t value);
 EIS_API int64_t eis_get_option(const char *key);
 

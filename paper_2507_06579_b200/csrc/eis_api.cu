@@ -59,11 +59,11 @@ struct Ctx {
                                      // at every d <= 1e11 on B200)
     int alpha_x16 = 16;              // BSGS baby window W = alpha * d^(1/4)
     int segment_log2 = 25;
-    int blocks_per_sm = 8;
+    int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
     int threads = 256;
     int baby_l2_mb = 64;
     int giant_ctas = 0;
-    int half_ksteps = 36;
+    int half_ksteps = 0;             // 0: chosen per segment from d
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
@@ -278,7 +278,14 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
             used_aux = true;
         } else {
             const unsigned wblocks = (unsigned)(g.num_sms * g.blocks_per_sm);
-            switch (g.half_ksteps) {
+            // chunk length: ~1/8 of the expected half period (~0.07 sqrt d steps),
+            // so lanes rarely idle after an exit (option half_ksteps = 0: auto)
+            int ks = g.half_ksteps;
+            if (ks == 0) {
+                const double exp_steps = 0.07 * std::sqrt((double)cand_d(seg));
+                ks = exp_steps >= 8 * 144 ? 144 : exp_steps >= 8 * 72 ? 72 : exp_steps >= 8 * 36 ? 36 : 18;
+            }
+            switch (ks) {
                 case 18: walk_half_kernel<18><<<wblocks, 256, 0, s>>>(a); break;
                 case 72: walk_half_kernel<72><<<wblocks, 256, 0, s>>>(a); break;
                 case 144: walk_half_kernel<144><<<wblocks, 256, 0, s>>>(a); break;
@@ -441,8 +448,8 @@ int eis_set_option(const char *key, int64_t v) {
         if (v < 0 || v > 32) return fail(EIS_EINVAL, "giant_ctas must be in [0, 32]");
         g.giant_ctas = (int)v;
     } else if (k == "half_ksteps") {
-        if (v != 18 && v != 36 && v != 72 && v != 144)
-            return fail(EIS_EINVAL, "half_ksteps must be 18, 36, 72 or 144");
+        if (v != 0 && v != 18 && v != 36 && v != 72 && v != 144)
+            return fail(EIS_EINVAL, "half_ksteps must be 0 (auto), 18, 36, 72 or 144");
         g.half_ksteps = (int)v;
     } else if (k == "blocks_per_sm") {
         if (v < 1 || v > 32) return fail(EIS_EINVAL, "blocks_per_sm must be in [1, 32]");
