@@ -125,6 +125,18 @@ EIS_API int eis_count(const uint64_t *x, size_t n, uint64_t *pi_D, uint64_t *pi_
 EIS_API int eis_count_window(uint64_t lo, const uint64_t *x, size_t n, uint64_t *cnt_D,
                      uint64_t *cnt_E);
 
+/* Extended counts: the prime subsequence (Sec. 3.2, l.501-522) and
+ * the residue classes.  out is a row-major [EIS_NROWS][n] host array:
+ *   out[0*n+i] = #{d in D : lo < d <= x[i]}
+ *   out[1*n+i] = #{d in E : ...}                      (t(eps_d) = 0)
+ *   out[2*n+i] = #{d in D with t(eps_d) = 1 : ...}    (t = 2 is row 0 - row 1 - row 2)
+ *   out[3*n+i] = #{d in D, d prime : ...}             (pi_{D cap P})
+ *   out[4*n+i] = #{d in E, d prime : ...}             (pi_{E cap P}, l.503-507)
+ * Same argument rules as eis_count_window; primality is decided by the
+ * sieve kernel (every odd prime p <= sqrt(x[n-1])). */
+#define EIS_NROWS 5
+EIS_API int eis_count_window_ext(uint64_t lo, const uint64_t *x, size_t n, uint64_t *out);
+
 /* ---- device-resident variants (multi-GPU path: one process per GPU) ---- */
 
 /* Accumulate per-bucket counts of d in (lo, hi] into bucket_dev[0..2n-1]:

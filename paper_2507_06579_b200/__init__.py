@@ -18,7 +18,8 @@ import numpy as np
 
 __all__ = [
     "EisError", "load", "init", "finalize", "set_option", "get_option", "num_candidates",
-    "classify_range", "count", "count_window", "count_buckets_dev", "prefix_dev",
+    "classify_range", "count", "count_window", "count_window_ext", "count_buckets_dev",
+    "prefix_dev",
     "classify_range_dev", "get_stats", "MODE_AUTO", "MODE_HALF", "MODE_BSGS", "NOT_IN_D",
     "MAX_D", "LIB_PATH",
 ]
@@ -35,7 +36,10 @@ EXPORTS = (
     "eis_init", "eis_finalize", "eis_last_error", "eis_set_option", "eis_get_option",
     "eis_num_candidates", "eis_classify_range", "eis_count", "eis_count_window",
     "eis_count_buckets_dev", "eis_prefix_dev", "eis_classify_range_dev", "eis_get_stats",
+    "eis_count_window_ext",
 )
+NROWS = 5
+ROW_NAMES = ("D", "E", "T1", "DP", "EP")
 
 
 class EisError(RuntimeError):
@@ -92,6 +96,8 @@ def load() -> ctypes.CDLL:
     L.eis_count.restype = c_int
     L.eis_count_window.argtypes = [u64, vp, sz, vp, vp]
     L.eis_count_window.restype = c_int
+    L.eis_count_window_ext.argtypes = [u64, vp, sz, vp]
+    L.eis_count_window_ext.restype = c_int
     L.eis_count_buckets_dev.argtypes = [u64, u64, vp, sz, vp, vp]
     L.eis_count_buckets_dev.restype = c_int
     L.eis_prefix_dev.argtypes = [vp, sz, vp, vp]
@@ -159,6 +165,15 @@ def count_window(lo: int, x) -> tuple[np.ndarray, np.ndarray]:
     cE = np.zeros(len(x), dtype=np.uint64)
     _check(load().eis_count_window(lo, x.ctypes.data, len(x), cD.ctypes.data, cE.ctypes.data))
     return cD, cE
+
+
+def count_window_ext(lo: int, x) -> dict:
+    """Rows D, E, T1 (t=1), DP (primes in D), EP (primes in E) over lo < d <= x_i
+    (Sec. 3.2); T2 = D - E - T1."""
+    x = _u64(x)
+    out = np.zeros((NROWS, len(x)), dtype=np.uint64)
+    _check(load().eis_count_window_ext(lo, x.ctypes.data, len(x), out.ctypes.data))
+    return dict(zip(ROW_NAMES, out))
 
 
 def _stream_handle(stream) -> int | None:

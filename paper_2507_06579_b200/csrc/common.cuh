@@ -104,6 +104,14 @@ EIS_HD u32 isqrt_u64_dev(u64 d) {
 // Segment-local checkpoint histogram capacity (buckets per segment).
 constexpr int HIST_CAP = 1024;
 
+// Count rows of the checkpoint histogram (eis_count_window_ext):
+//   0 D, 1 E (t = 0), 2 t = 1, 3 D cap P (prime d), 4 E cap P.
+// The basic counting functions use rows 0-1 only.
+constexpr int NROW_MAX = 5;
+// Survivor-list entries: bit 31 flags a prime d (set only when the sieve
+// was asked for primality); the low 31 bits are the segment offset.
+constexpr u32 PRIME_BIT = 0x80000000u;
+
 // Arguments shared by the walk kernels.
 struct WalkArgs {
     u64 i0;              // candidate index of segment offset 0
@@ -114,7 +122,8 @@ struct WalkArgs {
     const u64 *ckpt;     // nullable: checkpoints x[0..n_ckpt)
     int b_lo, nb;        // bucket range of this segment: [b_lo, b_lo+nb)
     int n_ckpt;
-    u64 *buckets;        // device: [n_ckpt] D counts then [n_ckpt] E counts
+    int nrow;            // count rows (2 or NROW_MAX)
+    u64 *buckets;        // device: [nrow][n_ckpt] counts (row order above)
     u64 *stats;          // device: EisStatSlot counters
     u32 *err;            // device: invariant-violation counter
 };
@@ -132,6 +141,37 @@ __device__ __forceinline__ int bucket_of(const u64 *x, int lo, int hi, u64 d) {
     }
     return lo;
 }
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void hist_zero(const WalkArgs &a, u32 *hist) {
+    for (int i = threadIdx.x; i < a.nrow * a.nb; i += blockDim.x) hist[i] = 0;
+}
+// K4: one finished d into the CTA's shared-memory histogram
+__device__ __forceinline__ void hist_record(const WalkArgs &a, u32 *hist, u64 d, u32 t,
+                                            bool prime) {
+    const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
+    atomicAdd(&hist[b], 1u);
+    if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
+    if (a.nrow > 2) {
+        if (t == 1) atomicAdd(&hist[2 * a.nb + b], 1u);
+        if (prime) {
+            atomicAdd(&hist[3 * a.nb + b], 1u);
+            if (t == 0) atomicAdd(&hist[4 * a.nb + b], 1u);
+        }
+    }
+}
+// one global atomic per CTA per nonzero bucket
+__device__ __forceinline__ void hist_flush(const WalkArgs &a, u32 *hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.nrow * a.nb; i += blockDim.x) {
+        if (hist[i]) {
+            const int r = i / a.nb, b = i - r * a.nb;
+            atomicAdd((unsigned long long *)&a.buckets[(size_t)r * a.n_ckpt + a.b_lo + b],
+                      (unsigned long long)hist[i]);
+        }
+    }
+}
+#endif
 
 __device__ __forceinline__ u32 lanemask_lt() {
     u32 m;

@@ -153,7 +153,7 @@ int do_init(int device) {
     for (auto &ev : g.ev) CUDA_TRY(cudaEventCreate(&ev));
     CUDA_TRY(cudaFuncSetAttribute(sieve_compact_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  SIEVE_WORDS * (int)sizeof(u32)));
+                                  2 * SIEVE_WORDS * (int)sizeof(u32)));
     g.inited = true;
     return 0;
 }
@@ -188,9 +188,11 @@ bool want_bsgs(u64 d_lo) {
 // Process candidates [i_first, i_last].  flags_dev (nullable) is indexed by
 // candidate index - i_first.  x_host/x_dev/n/buckets_dev (nullable) receive counts.
 int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u64 *x_dev,
-              int n, u64 *buckets_dev, cudaStream_t s) {
+              int n, u64 *buckets_dev, cudaStream_t s, int nrow = 2) {
+    const int with_primes = nrow > 2;
     const u64 SEG = 1ull << g.segment_log2;
     const int n_small = primes_small();
+    const int n_small1 = primes_upto_sq((u64)SIEVE_CHUNK * SIEVE_CHUNK / (64 * 64));   // p <= chunk/64
     // BSGS keeps one store per survivor of the segment (two segment buffers):
     // cap the segment so the stores stay within ~12 GB of HBM per buffer.
     const bool bsgs = want_bsgs(cand_d(i_first));
@@ -237,8 +239,10 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         CUDA_TRY(cudaMemsetAsync(bf.ctr, 0, 8 * sizeof(u32), s));
         const unsigned sblocks = (unsigned)((len + SIEVE_CHUNK - 1) / SIEVE_CHUNK);
         u8 *fseg = flags_dev ? flags_dev + (seg - i_first) : nullptr;
-        sieve_compact_kernel<<<sblocks, SIEVE_THREADS, SIEVE_WORDS * sizeof(u32), s>>>(
-            seg, len, g.d_primes, std::min(n_small, n_primes), n_primes, bf.list, bf.ctr, fseg);
+        sieve_compact_kernel<<<sblocks, SIEVE_THREADS,
+                               (with_primes ? 2 : 1) * SIEVE_WORDS * sizeof(u32), s>>>(
+            seg, len, g.d_primes, std::min(n_small, n_primes), n_primes, bf.list, bf.ctr, fseg,
+            with_primes, std::min(n_small1, n_primes));
         CUDA_TRY(cudaGetLastError());
         g.launches++;
 
@@ -253,6 +257,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.b_lo = b_lo;
         a.nb = nb;
         a.n_ckpt = n;
+        a.nrow = nrow;
         a.buckets = buckets_dev;
         a.stats = g.d_stats;
         if (bsgs) {
@@ -312,10 +317,10 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     return 0;
 }
 
-__global__ void prefix_kernel(const u64 *in, u64 *out, int n) {
-    // one CTA of 1024 threads: two independent inclusive scans of length n
+__global__ void prefix_kernel(const u64 *in, u64 *out, int n, int nrow) {
+    // one CTA of 1024 threads: nrow independent inclusive scans of length n
     __shared__ u64 part[1024];
-    for (int arr = 0; arr < 2; arr++) {
+    for (int arr = 0; arr < nrow; arr++) {
         const u64 *src = in + (size_t)arr * n;
         u64 *dst = out + (size_t)arr * n;
         const int per = (n + 1023) / 1024;
@@ -378,14 +383,34 @@ int check_x(const u64 *x, size_t n, u64 lo) {
     return 0;
 }
 
-int count_buckets(u64 lo, u64 hi, const u64 *x, size_t n, u64 *buckets_dev, cudaStream_t s) {
+int count_buckets(u64 lo, u64 hi, const u64 *x, size_t n, u64 *buckets_dev, cudaStream_t s,
+                  int nrow = 2) {
     if (n == 0 || hi <= lo) return 0;
     if (ensure(g.d_x, g.x_cap, n)) return EIS_ENOMEM;
     CUDA_TRY(cudaMemcpyAsync(g.d_x, x, n * sizeof(u64), cudaMemcpyHostToDevice, s));
     u64 top = std::min(hi, x[n - 1]);
     u64 i_first, i_last;
     if (!cand_range(lo + 1, top, i_first, i_last)) return 0;
-    return run_range(i_first, i_last, nullptr, x, g.d_x, (int)n, buckets_dev, s);
+    return run_range(i_first, i_last, nullptr, x, g.d_x, (int)n, buckets_dev, s, nrow);
+}
+
+// counts over (lo, x[n-1]] into host out[nrow][n] (prefix sums at checkpoints)
+int count_window_rows(u64 lo, const u64 *x, size_t n, int nrow, u64 *out) {
+    if (n == 0) return 0;
+    if (int rc = check_x(x, n, lo)) return rc;
+    if (!out) return fail(EIS_EINVAL, "NULL output");
+    if (int rc = do_init(-1)) return rc;
+    cudaStream_t s = g.stream;
+    if (int rc = begin_call(s)) return rc;
+    const size_t m = (size_t)nrow * n;
+    if (ensure(g.d_buckets, g.buckets_cap, m)) return EIS_ENOMEM;
+    CUDA_TRY(cudaMemsetAsync(g.d_buckets, 0, m * sizeof(u64), s));
+    if (int rc = count_buckets(lo, x[n - 1], x, n, g.d_buckets, s, nrow)) return rc;
+    prefix_kernel<<<1, 1024, 0, s>>>(g.d_buckets, g.d_buckets, (int)n, nrow);
+    CUDA_TRY(cudaGetLastError());
+    g.launches++;
+    CUDA_TRY(cudaMemcpyAsync(out, g.d_buckets, m * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    return end_call(s);
 }
 
 }  // namespace
@@ -539,7 +564,7 @@ int eis_prefix_dev(const uint64_t *bucket_dev, size_t n, uint64_t *out_dev, void
     if (!bucket_dev || !out_dev) return fail(EIS_EINVAL, "NULL pointer");
     if (int rc = do_init(-1)) return rc;
     cudaStream_t s = stream ? (cudaStream_t)stream : 0;
-    prefix_kernel<<<1, 1024, 0, s>>>(bucket_dev, out_dev, (int)n);
+    prefix_kernel<<<1, 1024, 0, s>>>(bucket_dev, out_dev, (int)n, 2);
     CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -547,23 +572,16 @@ int eis_prefix_dev(const uint64_t *bucket_dev, size_t n, uint64_t *out_dev, void
 int eis_count_window(uint64_t lo, const uint64_t *x, size_t n, uint64_t *cnt_D,
                      uint64_t *cnt_E) {
     if (n == 0) return 0;
-    if (int rc = check_x(x, n, lo)) return rc;
     if (!cnt_D || !cnt_E) return fail(EIS_EINVAL, "NULL output");
-    if (int rc = do_init(-1)) return rc;
-    cudaStream_t s = g.stream;
-    if (int rc = begin_call(s)) return rc;
-    if (ensure(g.d_buckets, g.buckets_cap, 2 * n)) return EIS_ENOMEM;
-    CUDA_TRY(cudaMemsetAsync(g.d_buckets, 0, 2 * n * sizeof(u64), s));
-    if (int rc = count_buckets(lo, x[n - 1], x, n, g.d_buckets, s)) return rc;
-    prefix_kernel<<<1, 1024, 0, s>>>(g.d_buckets, g.d_buckets, (int)n);
-    CUDA_TRY(cudaGetLastError());
-    g.launches++;
     std::vector<u64> h(2 * n);
-    CUDA_TRY(cudaMemcpyAsync(h.data(), g.d_buckets, 2 * n * sizeof(u64), cudaMemcpyDeviceToHost, s));
-    if (int rc = end_call(s)) return rc;
+    if (int rc = count_window_rows(lo, x, n, 2, h.data())) return rc;
     std::memcpy(cnt_D, h.data(), n * sizeof(u64));
     std::memcpy(cnt_E, h.data() + n, n * sizeof(u64));
     return 0;
+}
+
+int eis_count_window_ext(uint64_t lo, const uint64_t *x, size_t n, uint64_t *out) {
+    return count_window_rows(lo, x, n, EIS_NROWS, out);
 }
 
 int eis_count(const uint64_t *x, size_t n, uint64_t *pi_D, uint64_t *pi_E) {

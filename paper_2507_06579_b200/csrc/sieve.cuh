@@ -10,6 +10,11 @@
 //  * survivors are compacted with popc + a CTA scan and ONE global atomic per
 //    CTA into the segment's survivor list (u32 offsets within the segment).
 // Non-survivor flags (EIS_NOT_IN_D = 0xFF) are written with 16-byte stores.
+//
+// With `primes` set (the prime subsequence, Sec. 3.2 l.501-522), a
+// second bitmap marks the prime candidates: every odd prime p <= sqrt(d_max)
+// strikes its multiples d = p m >= p^2 (d = 5 mod 8 <=> i = r_p mod p with
+// r_p = -5/8 mod p), and survivors carry PRIME_BIT in their list entry.
 #pragma once
 #include "common.cuh"
 
@@ -20,8 +25,10 @@ constexpr int SIEVE_WPT = SIEVE_WORDS / SIEVE_THREADS;   // bitmap words per thr
 
 __global__ void __launch_bounds__(SIEVE_THREADS)
 sieve_compact_kernel(u64 i0, u64 len, const u32 *__restrict__ primes, int n_small, int n_primes,
-                     u32 *__restrict__ list, u32 *__restrict__ count, u8 *__restrict__ flags) {
+                     u32 *__restrict__ list, u32 *__restrict__ count, u8 *__restrict__ flags,
+                     int with_primes, int n_small1) {
     extern __shared__ u32 bm[];
+    u32 *pm = bm + SIEVE_WORDS;                   // primality bitmap (with_primes)
     __shared__ u32 warp_tot[SIEVE_THREADS / 32];
     __shared__ u32 blk_base;
     const int tid = threadIdx.x;
@@ -35,6 +42,7 @@ sieve_compact_kernel(u64 i0, u64 len, const u32 *__restrict__ primes, int n_smal
         if (lo + 32 <= clen) v = FULL_MASK;
         else if (lo < clen) v = (1u << (clen - lo)) - 1;
         bm[w] = v;
+        if (with_primes) pm[w] = v;
     }
     __syncthreads();
 
@@ -54,6 +62,34 @@ sieve_compact_kernel(u64 i0, u64 len, const u32 *__restrict__ primes, int n_smal
         u64 r = (5 * p2 - 5) / 8;
         u64 off = (r + p2 - base % p2) % p2;
         if (off < clen) atomicAnd(&bm[off >> 5], ~(1u << (off & 31)));
+    }
+    if (with_primes) {
+        // multiples d = p m, m >= p (so p itself stays prime), of every odd
+        // prime p <= sqrt(d_max): i = r_p (mod p), i >= (p^2 - 1)/8
+        auto first_strike = [&](u32 p) -> u64 {      // offset of the first strike, or >= clen
+            const u32 inv8 = (u32)((1 + (u64)p * ((8 - p % 8) % 8)) / 8);   // 8^-1 mod p
+            u32 r5 = 5 * inv8;                                               // < 5p
+            while (r5 >= p) r5 -= p;
+            const u32 rp = r5 ? p - r5 : 0;                                  // -5/8 mod p
+            const u64 i_min = ((u64)p * p - 1) / 8;
+            const u64 f0 = base > i_min ? base : i_min;
+            u64 q = (u64)((double)f0 / (double)p);                           // f0 < 2^34: exact
+            while (q * p > f0) q--;
+            while ((q + 1) * p <= f0) q++;
+            const u32 fm = (u32)(f0 - q * p);                                // f0 mod p
+            const u64 first = f0 + (rp >= fm ? rp - fm : rp + p - fm);
+            return first - base;
+        };
+        for (int k = 0; k < n_small1; k++) {          // many strikes per chunk: whole CTA
+            const u32 p = primes[k];
+            const u64 j0 = first_strike(p);
+            for (u64 j = j0 + (u64)tid * p; j < clen; j += (u64)SIEVE_THREADS * p)
+                atomicAnd(&pm[j >> 5], ~(1u << (j & 31)));
+        }
+        for (int k = n_small1 + tid; k < n_primes; k += SIEVE_THREADS) {   // few strikes each
+            const u32 p = primes[k];
+            for (u64 j = first_strike(p); j < clen; j += p) atomicAnd(&pm[j >> 5], ~(1u << (j & 31)));
+        }
     }
     __syncthreads();
 
@@ -91,7 +127,8 @@ sieve_compact_kernel(u64 i0, u64 len, const u32 *__restrict__ primes, int n_smal
         while (bits) {
             int b = __ffs(bits) - 1;
             bits &= bits - 1;
-            list[pos++] = o + b;
+            const u32 pb = with_primes ? ((pm[w0 + w] >> b) & 1u) << 31 : 0u;
+            list[pos++] = (o + b) | pb;
         }
     }
     if (flags) {

@@ -428,28 +428,11 @@ struct BsgsOut {
 };
 
 #ifdef __CUDACC__
-__device__ __forceinline__ void record_result(const WalkArgs &a, u32 *hist, u32 off, u64 d,
+__device__ __forceinline__ void record_result(const WalkArgs &a, u32 *hist, u32 le, u64 d,
                                               u32 res) {
     const u32 t = res % 3;
-    if (a.flags) a.flags[off] = (u8)t;
-    if (a.ckpt) {
-        const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
-        atomicAdd(&hist[b], 1u);
-        if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
-    }
-}
-
-__device__ __forceinline__ void flush_hist(const WalkArgs &a, u32 *hist) {
-    __syncthreads();
-    if (a.ckpt) {
-        for (int i = threadIdx.x; i < a.nb; i += blockDim.x) {
-            if (hist[i])
-                atomicAdd((unsigned long long *)&a.buckets[a.b_lo + i], (unsigned long long)hist[i]);
-            if (hist[a.nb + i])
-                atomicAdd((unsigned long long *)&a.buckets[a.n_ckpt + a.b_lo + i],
-                          (unsigned long long)hist[a.nb + i]);
-        }
-    }
+    if (a.flags) a.flags[le & ~PRIME_BIT] = (u8)t;
+    if (a.ckpt) hist_record(a, hist, d, t, (le & PRIME_BIT) != 0);
 }
 
 __device__ __forceinline__ void flush_stats(const WalkArgs &a, u64 baby, u64 giant, u64 red,
@@ -474,9 +457,9 @@ template <int KB>
 __global__ void __launch_bounds__(256)
 bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     extern __shared__ u32 smem[];
-    u32 *hist = smem;                              // 2 * HIST_CAP
-    u32 *bmap = smem + 2 * HIST_CAP;               // (ns/32) words x blockDim
-    for (int i = threadIdx.x; i < 2 * a.nb; i += blockDim.x) hist[i] = 0;
+    u32 *hist = smem;                              // NROW_MAX * HIST_CAP
+    u32 *bmap = smem + NROW_MAX * HIST_CAP;        // (ns/32) words x blockDim
+    hist_zero(a, hist);
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -505,11 +488,11 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         ln.phase = PH_IDLE;
         u32 off = 0;
         if (idx < n) {
-            off = __ldg(a.list + idx);
+            off = __ldg(a.list + idx);            // (with the prime bit)
             S.tab = o.tables + ((u64)idx << B.ns_log2);
             S.list = o.lists + (u64)idx * o.lcap;
             baby += 1;
-            if (bsgs_begin(ln, S, B, cand_d(a.i0 + off))) {
+            if (bsgs_begin(ln, S, B, cand_d(a.i0 + (off & ~PRIME_BIT)))) {
                 record_result(a, hist, off, ln.d, ln.res);
                 done++;
                 sym++;
@@ -550,13 +533,13 @@ bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
     }
     flush_stats(a, baby, giant, red, done, sym, 0, err);
-    flush_hist(a, hist);
+    hist_flush(a, hist);
 }
 
 __global__ void __launch_bounds__(256)
 bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
-    __shared__ u32 hist[2 * HIST_CAP];
-    for (int i = threadIdx.x; i < 2 * a.nb; i += blockDim.x) hist[i] = 0;
+    __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    hist_zero(a, hist);
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -581,8 +564,8 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 if (qi < nq) {
                     const u32 idx = __ldg(o.queue + qi);
                     const GiantRec r = o.recs[idx];
-                    off = r.off;
-                    giant_unpack(g, r, cand_d(a.i0 + off));
+                    off = r.off;                          // (with the prime bit)
+                    giant_unpack(g, r, cand_d(a.i0 + (off & ~PRIME_BIT)));
                     pending = true;               // mu'_2 is probed with the next advance
                     tab = o.tables + ((u64)idx << B.ns_log2);
                     list = o.lists + (u64)idx * o.lcap;
@@ -637,7 +620,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
     }
     flush_stats(a, baby, giant, red, done, 0, fb, err);
-    flush_hist(a, hist);
+    hist_flush(a, hist);
 }
 
 // ------------------------------------------------------------- host launch --
@@ -726,7 +709,7 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     // read-modify-write traffic otherwise).
     const size_t store_bytes = (size_t)4 << B.ns_log2;
     const int bt = BSGS_THREADS;
-    pl.baby_smem = (size_t)(2 * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * bt * 4;
+    pl.baby_smem = (size_t)(NROW_MAX * HIST_CAP) * 4 + (size_t)(1 << B.ns_log2) / 32 * bt * 4;
     if (cudaFuncSetAttribute(bsgs_baby_kernel<BSGS_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pl.baby_smem) != cudaSuccess)
         return -4;

@@ -143,8 +143,8 @@ EIS_HD u32 half_step_cap(u32 s) { return 48u * s + 64u; }
 template <int KSTEPS>
 __global__ void __launch_bounds__(256)
 walk_half_kernel(WalkArgs a) {
-    __shared__ u32 hist[2 * HIST_CAP];
-    for (int i = threadIdx.x; i < 2 * a.nb; i += blockDim.x) hist[i] = 0;
+    __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    hist_zero(a, hist);
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -153,6 +153,7 @@ walk_half_kernel(WalkArgs a) {
     BabyStateF st;
     u64 d = 0;
     u32 off = 0;
+    bool prime = false;
     bool active = false, exhausted = false;
     u32 n_done = 0, n_sym = 0, n_err = 0, dsteps = 0, cap = 0;
     u64 steps = 0;
@@ -162,11 +163,7 @@ walk_half_kernel(WalkArgs a) {
         n_done++;
         n_sym++;
         if (a.flags) a.flags[off] = (u8)t;
-        if (a.ckpt) {
-            const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
-            atomicAdd(&hist[b], 1u);
-            if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
-        }
+        if (a.ckpt) hist_record(a, hist, d, t, prime);
     };
 
     for (;;) {
@@ -179,7 +176,9 @@ walk_half_kernel(WalkArgs a) {
             if (!active && !exhausted) {
                 const u32 idx = base + __popc(need & lanemask_lt());
                 if (idx < n) {
-                    off = __ldg(a.list + idx);
+                    const u32 le = __ldg(a.list + idx);
+                    off = le & ~PRIME_BIT;
+                    prime = (le & PRIME_BIT) != 0;
                     d = cand_d(a.i0 + off);
                     u32 r1;
                     if (baby_init(st0, d, &r1)) {
@@ -227,14 +226,5 @@ walk_half_kernel(WalkArgs a) {
         atomicAdd((unsigned long long *)&a.stats[ST_D], (unsigned long long)s_done);
         atomicAdd((unsigned long long *)&a.stats[ST_SYM], (unsigned long long)s_sym);
     }
-    __syncthreads();
-    if (a.ckpt) {
-        for (int i = threadIdx.x; i < a.nb; i += blockDim.x) {
-            if (hist[i])
-                atomicAdd((unsigned long long *)&a.buckets[a.b_lo + i], (unsigned long long)hist[i]);
-            if (hist[a.nb + i])
-                atomicAdd((unsigned long long *)&a.buckets[a.n_ckpt + a.b_lo + i],
-                          (unsigned long long)hist[a.nb + i]);
-        }
-    }
+    if (a.ckpt) hist_flush(a, hist);
 }

@@ -52,3 +52,24 @@ def pi_D_closed_form(x: int) -> int:
         if mu[m]:
             tot += int(mu[m]) * ((x // (m * m) + 3) // 8)
     return tot
+
+
+def prime_mask(lo: int, hi: int) -> np.ndarray:
+    """is_prime[k] for the integers lo + k, lo <= lo + k <= hi, by a plain
+    segmented Eratosthenes (independent of the oracle and of the CUDA sieve)."""
+    n = hi - lo + 1
+    mask = np.ones(n, dtype=bool)
+    r = isqrt(hi)
+    small = np.ones(r + 1, dtype=bool)
+    small[:2] = False
+    for p in range(2, isqrt(r) + 1):
+        if small[p]:
+            small[p * p::p] = False
+    for p in np.flatnonzero(small):
+        p = int(p)
+        start = max(p * p, ((lo + p - 1) // p) * p)
+        mask[start - lo::p] = False
+    for v in (0, 1):
+        if lo <= v <= hi:
+            mask[v - lo] = False
+    return mask

@@ -200,3 +200,29 @@ def test_metric_slab_as_benched():
     got = f[((s - (lo + 1 + (5 - (lo + 1)) % 8)) // 8).astype(np.int64)]
     want = c_oracle.classify_list(s, NTHREADS)
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------- prime subsequence, residue classes --
+@pytest.mark.parametrize("lo,hi", [(0, 10**6), (10**9 - 2 * 10**5 - 3, 10**9 + 11)])
+def test_count_window_ext_rows(mode, lo, hi):
+    """eis_count_window_ext (Sec. 3.2, l.501-522): D, E, t=1, primes in D
+    and primes in E, against the oracle's per-d t and an independent sieve."""
+    from pins import prime_mask
+
+    x = [lo + (hi - lo) // 3, lo + (hi - lo) // 2 + 1, hi]
+    rows = eis.count_window_ext(lo, x)
+    cD, cE = eis.count_window(lo, x)
+    assert np.array_equal(rows["D"], cD) and np.array_equal(rows["E"], cE)
+    f = c_oracle.classify_range(lo + 1, hi, NTHREADS)
+    first = (lo + 1) + (5 - (lo + 1)) % 8
+    d = first + 8 * np.arange(f.size, dtype=np.int64)
+    pm = prime_mask(lo + 1, hi)[d - (lo + 1)]
+    for i, xi in enumerate(x):
+        m = d <= xi
+        inD = m & (f != c_oracle.NOT_IN_D)
+        assert int(rows["D"][i]) == int(inD.sum())
+        assert int(rows["E"][i]) == int((m & (f == 0)).sum())
+        assert int(rows["T1"][i]) == int((m & (f == 1)).sum())
+        assert int(rows["DP"][i]) == int((inD & pm).sum())
+        assert int(rows["EP"][i]) == int((m & (f == 0) & pm).sum())
+    assert int(rows["DP"][-1]) > 0 and int(rows["EP"][-1]) > 0
