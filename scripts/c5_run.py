@@ -1,8 +1,12 @@
-"""BASELINE config C5 on ONE B200: pi_D, pi_E at every 1e7 up to 1e11.
+"""BASELINE config C5 on ONE B200: all rows at every 1e7 up to 1e11.
 
-Checks every Table 1 total as checkpoint differences,
-pi_D against the Moebius closed form, and fits eq. (1):
-pi_E(x) ~ x/(3 pi^2) + c x^(5/6), the paper reports c ~ -0.024.
+Rows (eis_count_window_ext): D, E, t=1, D cap P, E cap P.  Checks every Table 1
+total as checkpoint differences and pi_D against the
+Moebius closed form; fits
+  eq. (1)   pi_E(x) ~ x/(3 pi^2) + c x^(5/6)                 (c ~ -0.024)
+  eq. (pdata) pi_{E cap P}(x) ~ pi(x)/12 + a int_2^x dt/(t^(1/6) ln t)
+            (l.503-507, a ~ -0.037), with pi(x)/12 ~ pi_{D cap P}(x)/3
+            (primes = 5 mod 8 are pi(x)/4 up to lower-order terms).
 Writes profiles/r01_c5_checkpoints.csv and prints a JSON summary."""
 import json, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -17,33 +21,48 @@ top = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10**11
 stride = 10**7
 x = np.arange(stride, top + 1, stride, dtype=np.uint64)
 t0 = time.time()
-pD, pE = eis.count(x)
+R = eis.count_window_ext(0, x)
 wall = time.time() - t0
 st = eis.get_stats()
 out = os.path.join(ROOT, "profiles", "r01_c5_checkpoints.csv")
 with open(out, "w") as f:
-    f.write("x,pi_D,pi_E\n")
-    for a, b, c in zip(x, pD, pE):
-        f.write(f"{int(a)},{int(b)},{int(c)}\n")
+    f.write("x,pi_D,pi_E,pi_T1,pi_DP,pi_EP\n")
+    for i, a in enumerate(x):
+        f.write(f"{int(a)},{int(R['D'][i])},{int(R['E'][i])},{int(R['T1'][i])},"
+                f"{int(R['DP'][i])},{int(R['EP'][i])}\n")
 idx = {int(v): i for i, v in enumerate(x)}
-def at(arr, v):
-    return 0 if v == 0 else int(arr[idx[v]])
+def at(row, v):
+    return 0 if v == 0 else int(R[row][idx[v]])
 table1 = []
 for lo, hi, want in paper_windows():
     if hi <= top:
-        got = at(pE, hi) - at(pE, lo)
+        got = at("E", hi) - at("E", lo)
         table1.append({"window": [lo, hi], "E": got, "paper": want, "ok": got == want})
-moeb = {str(v): (at(pD, v), pi_D_closed_form(v)) for v in [10**8, 10**9, 10**10, top] if v <= top}
-# least-squares fit of pi_E(x) - x/(3 pi^2) = c x^(5/6) on x >= 1e8
+moeb = {str(v): [at("D", v), pi_D_closed_form(v)] for v in [10**8, 10**9, 10**10, top] if v <= top}
 xs = x.astype(np.float64)
 m = xs >= 1e8
-r = pE.astype(np.float64)[m] - xs[m] / (3 * np.pi**2)
+# eq. (1)
+r = R["E"].astype(np.float64)[m] - xs[m] / (3 * np.pi**2)
 b = xs[m] ** (5 / 6)
 c = float((b @ r) / (b @ b))
-print(json.dumps({"top": top, "checkpoints": len(x), "wall_s": round(wall, 2),
-                  "device_ms": round(st["total_ms"], 1), "d_classified": st["d_classified"],
-                  "rate_d_per_s": st["d_classified"] / (st["total_ms"] / 1e3),
-                  "baby_steps": st["baby_steps"], "giant_steps": st["giant_steps"],
-                  "pi_D": at(pD, top), "pi_E": at(pE, top), "table1": table1,
-                  "moebius_pi_D": moeb, "fit_c_5_6": c, "paper_c": -0.024,
-                  "mode": eis.get_option("mode")}, indent=1))
+# eq. (pdata): I(x) = int_2^x dt / (t^(1/6) ln t), cumulative trapezoid on a log grid
+grid = np.unique(np.concatenate([np.geomspace(2, float(top), 200000), xs]))
+fgrid = 1.0 / (grid ** (1 / 6) * np.log(grid))
+I = np.concatenate([[0.0], np.cumsum(0.5 * (fgrid[1:] + fgrid[:-1]) * np.diff(grid))])
+Ix = np.interp(xs, grid, I)
+rp = R["EP"].astype(np.float64)[m] - R["DP"].astype(np.float64)[m] / 3.0
+a_fit = float((Ix[m] @ rp) / (Ix[m] @ Ix[m]))
+T2 = R["D"].astype(np.int64) - R["E"].astype(np.int64) - R["T1"].astype(np.int64)
+print(json.dumps({
+    "top": top, "checkpoints": len(x), "wall_s": round(wall, 2),
+    "device_ms": round(st["total_ms"], 1), "d_classified": st["d_classified"],
+    "rate_d_per_s": st["d_classified"] / (st["total_ms"] / 1e3),
+    "mode": eis.get_option("mode"),
+    "pi_D": at("D", top), "pi_E": at("E", top), "pi_T1": at("T1", top), "pi_T2": int(T2[-1]),
+    "pi_DP": at("DP", top), "pi_EP": at("EP", top),
+    "table1": table1, "moebius_pi_D": moeb,
+    "eq1_fit_c": c, "eq1_paper_c": -0.024,
+    "pdata_fit_a": a_fit, "pdata_paper_a": -0.037,
+    "share_E_in_D_at_top": at("E", top) / at("D", top),
+    "share_EP_in_DP_at_top": at("EP", top) / max(1, at("DP", top)),
+}, indent=1))
