@@ -167,6 +167,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo: orchestration test only)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="all ranks on cuda:0 (orchestration test on a 1-GPU box; the "
+                         "ranks' kernels never wait on one another)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -183,11 +188,15 @@ def main():
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched under torchrun")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    gpu = 0 if args.share_gpu else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    eis.init(local)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    eis.init(gpu)
     eis.set_option("mode", {"auto": eis.MODE_AUTO, "half": eis.MODE_HALF,
                             "bsgs": eis.MODE_BSGS}[args.mode])
 
@@ -213,8 +222,8 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     walk_ms, launches, stats = [], 0, {}
-    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]
-                               if os.environ.get("CUDA_VISIBLE_DEVICES") else local))
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    sampler = ClockSampler(int(cvd.split(",")[gpu]) if cvd else gpu)
     sampler.start()
     time.sleep(0.3)
     if world > 1:
