@@ -108,18 +108,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_baseline(lo: int, hi: int, seconds_target: float = 15.0, n: int | None = None) -> dict:
     """The oracle as it stands, on all host cores, on a seeded sample of the
-    workload (candidates of (lo, hi]); value in d/s (d in D only)."""
+    workload (candidates of (lo, hi]); value in d/s (d in D only).  The thread
+    count is passed explicitly (torchrun sets OMP_NUM_THREADS=1)."""
     from oracle import c_oracle
 
-    ncpu = os.cpu_count() or 1
+    ncpu = host_cores()
     # ~15 ms/d/core at 1e10 (measured), so ncpu*1000 candidates ~ 15 s
     n = n or max(64, int(ncpu * 1000 * seconds_target / 15.0))
     s = workloads.sample_candidates(lo + 1, hi, n, seed=workloads.SEED + 1)
     c_oracle.lib()
     t0 = time.perf_counter()
-    f = c_oracle.classify_list(s, 0)
+    f = c_oracle.classify_list(s, ncpu)
     dt = time.perf_counter() - t0
     nd = int((f != c_oracle.NOT_IN_D).sum())
     return {"value": nd / dt, "unit": UNIT, "cores": ncpu, "kind": "oracle",
@@ -134,7 +142,7 @@ def run_reference(args) -> None:
         return
     n_gpus = args.gpus
     lo, hi = workloads.metric_window(n_gpus)
-    ncpu = os.cpu_count() or 1
+    ncpu = host_cores()
     per_step = max(32, int(ncpu * 1000 * args.ref_seconds / 15.0))
     vals, times = [], []
     for k in range(args.warmup + args.steps):
@@ -299,7 +307,7 @@ def main():
             "e2e": {"value": nD_job / float(te[0]), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 16 * n,
                     "path": "eis_count_window (C ABI, host buffers)" if world == 1
-                    else "count_window_distributed (C ABI dev + NCCL allreduce)"},
+                    else f"count_window_distributed (C ABI dev + {args.backend} allreduce)"},
             "gpu_launches": launches,
             "roofline": {
                 "bound": "alu", "kernel": "walk (K3+K4)",
