@@ -95,7 +95,6 @@ EIS_API const char *eis_last_error(void);
  *  "alpha_x16"     BSGS baby window W = (alpha_x16/16) d^(1/4), in [4, 64]
  *  "segment_log2"  candidates per segment (HALF; BSGS caps it by store memory)
  *  "blocks_per_sm" HALF walk kernel CTAs per SM
- *  "baby_l2_mb"    BSGS baby kernel: MB of L2 its resident stores may occupy
  *  "giant_ctas"    BSGS giant kernel CTAs per SM (0 = occupancy maximum)
  *  "half_ksteps"   HALF walk: rho steps per lane between refills (0 = auto, 18/36/72/144) */
 EIS_API int eis_set_option(const char *key, int64_t value);

@@ -61,7 +61,6 @@ struct Ctx {
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
     int threads = 256;
-    int baby_l2_mb = 64;
     int giant_ctas = 0;
     int half_ksteps = 0;             // 0: chosen per segment from d
     // instrumentation of the last call
@@ -198,8 +197,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     const bool bsgs = want_bsgs(cand_d(i_first));
     u64 seg_cap = SEG;
     if (bsgs) {
-        const int nsl = bsgs_ns_log2(cand_d(i_last), g.alpha_x16 / 16.0f);
-        const u64 per = ((u64)4 << nsl) + ((u64)4 << nsl) / 2 + sizeof(GiantRec) + 4;
+        const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), g.alpha_x16 / 16.0f);
         seg_cap = std::min<u64>(SEG, std::max<u64>((12ull << 30) / per, 1ull << 16));
     }
     CUDA_TRY(cudaEventRecord(g.ev[2], s));
@@ -262,10 +260,9 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.stats = g.d_stats;
         if (bsgs) {
             BsgsPlan pl;
-            if (bf.bsgs.tables_bytes < ((size_t)(len + 32) << bsgs_ns_log2(d_last, g.alpha_x16 / 16.0f)))
-                CUDA_TRY(cudaDeviceSynchronize());          // (re)allocation below
-            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.baby_l2_mb,
-                                  g.giant_ctas, bf.bsgs, bf.ctr + 2);
+            CUDA_TRY(cudaStreamSynchronize(g.aux));     // scratch may be (re)allocated below
+            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.giant_ctas, bf.bsgs,
+                                  bf.ctr + 2);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -443,7 +440,6 @@ void eis_finalize(void) {
     fresh.alpha_x16 = g.alpha_x16;
     fresh.segment_log2 = g.segment_log2;
     fresh.blocks_per_sm = g.blocks_per_sm;
-    fresh.baby_l2_mb = g.baby_l2_mb;
     fresh.giant_ctas = g.giant_ctas;
     fresh.half_ksteps = g.half_ksteps;
     g = fresh;
@@ -466,9 +462,6 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "segment_log2") {
         if (v < 18 || v > 31) return fail(EIS_EINVAL, "segment_log2 must be in [18, 31]");
         g.segment_log2 = (int)v;
-    } else if (k == "baby_l2_mb") {
-        if (v < 1 || v > 4096) return fail(EIS_EINVAL, "baby_l2_mb must be in [1, 4096]");
-        g.baby_l2_mb = (int)v;
     } else if (k == "giant_ctas") {
         if (v < 0 || v > 32) return fail(EIS_EINVAL, "giant_ctas must be in [0, 32]");
         g.giant_ctas = (int)v;
@@ -493,7 +486,6 @@ int64_t eis_get_option(const char *key) {
     if (k == "alpha_x16") return g.alpha_x16;
     if (k == "segment_log2") return g.segment_log2;
     if (k == "blocks_per_sm") return g.blocks_per_sm;
-    if (k == "baby_l2_mb") return g.baby_l2_mb;
     if (k == "giant_ctas") return g.giant_ctas;
     if (k == "half_ksteps") return g.half_ksteps;
     return fail(EIS_EINVAL, "unknown option '%s'", key);

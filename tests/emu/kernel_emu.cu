@@ -25,7 +25,7 @@ int main(int argc, char **argv) {
     B.plain_th = argc > 4 ? atoi(argv[4]) : 50;
     B.giant_cap_mul = 20.0f;
     std::vector<u32> bm(1 << 10);
-    std::vector<u32> tab(1 << 14), lst(1 << 13);
+    std::vector<u32> tab(1 << 14), lst(1 << 12);
     unsigned long long d;
     while (scanf("%llu", &d) == 1) {
         u32 res = 0, err = 0;
@@ -44,41 +44,36 @@ int main(int argc, char **argv) {
                 res = baby_result_f(sf);
             }
         } else {
-            B.ns_log2 = ns_fixed ? ns_fixed : bsgs_ns_log2(d, B.alpha);
-            B.cap = (1 << B.ns_log2) / 2 - 2;
-            Store S;
-            S.bm = bm.data();
-            S.stride = 1;
-            S.tab = tab.data();
-            S.list = lst.data();
-            S.ns_log2 = B.ns_log2;
+            const BsgsSizes z = bsgs_sizes(d, B.alpha);
+            B.ns_log2 = ns_fixed ? ns_fixed : z.ns_log2;
+            B.cap = ns_fixed ? (1 << ns_fixed) / 2 - 2 : z.cap;
+            B.lcap = (B.cap + 31) & ~31;
             std::fill(tab.begin(), tab.begin() + (1 << B.ns_log2), 0u);
-            BsgsLane ln;
+            BabyLane ln;
             baby = 1;
-            bsgs_begin(ln, S, B, d);
-            while (ln.phase == PH_BABY) baby += bsgs_baby(ln, S, B, 8);
-            if (ln.phase == PH_DONE) {
+            if (bsgs_begin(ln, lst.data(), B, d)) {
                 res = ln.res;
             } else {
-                GiantLane g;
-                giant_init(g, B, ln.d, ln.Q1, ln.P1, ln.t1, ln.dist1, &err);
-                while (g.phase == PH_GIANT) {
-                    GiantInfo gi = bsgs_giant(g, S.tab, S.list, B, &err);
-                    giant++;
-                    red += gi.nred;
-                    kinds[gi.kind]++;
-                }
-                if (g.phase == PH_HALF) {
-                    fb++;
-                    BabyState st;
-                    u32 r1;
-                    if (baby_init(st, ln.d, &r1)) g.res = r1;
-                    else {
-                        do { baby++; } while (!baby_step(st));
-                        g.res = baby_result(st);
+                while (ln.phase == PH_BABY) baby += bsgs_baby(ln, lst.data(), B, 8);
+                if (ln.phase == PH_DONE) {
+                    res = ln.res;
+                } else {
+                    store_build_seq(tab.data(), B.ns_log2, lst.data(), ln.n);
+                    const BabyRec br = baby_pack(ln, 0);
+                    GiantLane g;
+                    giant_init(g, B, d, br, &err);
+                    while (g.phase == PH_GIANT) {
+                        GiantInfo gi = bsgs_giant(g, tab.data(), lst.data(), B, &err);
+                        giant++;
+                        red += gi.nred;
+                        kinds[gi.kind]++;
                     }
+                    if (g.phase == PH_HALF) {
+                        fb++;
+                        g.res = half_walk_one(d, baby, err);
+                    }
+                    res = g.res;
                 }
-                res = g.res;
             }
         }
         printf("%llu %u %llu %llu %llu %llu %u %llu %llu %llu\n", d, res % 3,
