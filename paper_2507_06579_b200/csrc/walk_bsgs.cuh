@@ -131,7 +131,8 @@ struct BabyLane {
     float dist;         // log2 theta_{j+1} of the current ideal
     float sqd_m;        // sqrt(d) - 2^23 (P + sqrt d = Pm + sqd_m)
     float W2;           // window in log2 units
-    u32 n;              // list entries written
+    u32 n;              // list entries (those of the last partial group are pending)
+    u32 pe0, pe1, pe2;  // pending entries of the group [n & ~3, n), not yet in memory
     int extras;         // -1 before the window is complete, then 2, 1
     u32 Q1, P1, t1;     // mu_1
     float dist1;
@@ -179,8 +180,10 @@ EIS_HD bool bsgs_begin(BabyLane &ln, u32 *list, const BsgsArgs &B, u64 d) {
     const float sqd = (float)sqrt((double)d);
     ln.sqd_m = sqd - 8388608.0f;
     ln.W2 = B.alpha * sqrtf(sqd) / LN2F;
-    list[0] = list_entry(2u, 0u);
-    list[1] = list_entry(b.Q, b.t2 >> 1);
+    (void)list;
+    ln.pe0 = list_entry(2u, 0u);                      // entries 0 and 1, written with
+    ln.pe1 = list_entry(b.Q, b.t2 >> 1);              // the first full group
+    ln.pe2 = 0;
     ln.dist = log2_approx(((float)b.P + sqd) * 0.5f);
     ln.n = 2;
     ln.extras = -1;
@@ -197,14 +200,35 @@ EIS_HD bool bsgs_begin(BabyLane &ln, u32 *list, const BsgsArgs &B, u64 d) {
 
 // Up to `kmax` baby steps (Alg. 1 l.549-561).  Sets PH_DONE (symmetry exit) or
 // PH_GIANT (window + two more ideals stored).  Returns the steps taken.
+// List entries are gathered four at a time in registers and written with one
+// 16-byte store (per-lane lists are 16-byte aligned); a 4-byte store per step
+// makes the kernel store-transaction bound (32 lines per warp instruction).
+EIS_HD void list_flush(u32 *list, u32 n, u32 e0, u32 e1, u32 e2, u32 e3) {
+    // entries n-? .. n-1 are pending: n % 4 of them (e0 oldest); at n % 4 == 0 all four
+    const u32 k = n & 3u, b = n - (k ? k : 4u);
+    if (k == 0) {
+        *reinterpret_cast<uint4 *>(list + b) = make_uint4(e0, e1, e2, e3);
+    } else {
+        list[b] = e0;
+        if (k > 1) list[b + 1] = e1;
+        if (k > 2) list[b + 2] = e2;
+    }
+}
+
 EIS_HD int bsgs_baby(BabyLane &ln, u32 *list, const BsgsArgs &B, int kmax) {
     int k = 0;
+    // pending group: entries [n & ~3, n) live in e0..e2 (list is written up to n & ~3)
+    u32 e0 = ln.pe0, e1 = ln.pe1, e2 = ln.pe2, e3 = 0;
     while (k < kmax) {
         const bool ex = baby_step_fd(ln.st, ln.sqd_m, ln.dist);
         k++;
-        list[ln.n] = list_entry(f_to_u(ln.st.Q), ln.st.t2 >> 1);
+        const u32 e = list_entry(f_to_u(ln.st.Q), ln.st.t2 >> 1);
+        const u32 p = ln.n & 3u;
+        if (p == 0) e0 = e; else if (p == 1) e1 = e; else if (p == 2) e2 = e; else e3 = e;
         ln.n++;
+        if (p == 3) list_flush(list, ln.n, e0, e1, e2, e3);
         if (ex) {
+            if ((ln.n & 3u) != 0) list_flush(list, ln.n, e0, e1, e2, e3);
             ln.res = baby_result_f(ln.st);
             ln.phase = PH_DONE;
             return k;
@@ -218,10 +242,14 @@ EIS_HD int bsgs_baby(BabyLane &ln, u32 *list, const BsgsArgs &B, int kmax) {
                 ln.extras = 2;                           // "Compute two more ideals" (l.560)
             }
         } else if (--ln.extras == 0) {
+            if ((ln.n & 3u) != 0) list_flush(list, ln.n, e0, e1, e2, e3);
             ln.phase = PH_GIANT;
             return k;
         }
     }
+    ln.pe0 = e0;                                    // chunk end: keep the group pending
+    ln.pe1 = e1;
+    ln.pe2 = e2;
     return k;
 }
 
@@ -532,12 +560,27 @@ bsgs_build_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         for (u32 q = 0; q < cnt; q++) {
             const u32 idx = __shfl_sync(FULL_MASK, myq, q);
             const u32 ne = o.brecs[idx].n;
-            const u32 *list = o.lists + (u64)idx * B.lcap;
-            for (u32 j = lane; j < ne; j += 32) {            // insert entries
-                const u32 e = list[j], Q = e & 0xFFFFFu;
-                const u32 v = slot_entry(Q, j, mod3(e >> 20));
-                u32 h = store_hash(Q, B.ns_log2);
-                while (atomicCAS(&tab[h], 0u, v) != 0u) h = (h + 1) & mask;
+            const uint4 *l4 = reinterpret_cast<const uint4 *>(o.lists + (u64)idx * B.lcap);
+            for (u32 jb = 0; jb < ne; jb += 512) {           // up to 4 x 16 B per lane in flight
+                uint4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const u32 j4 = jb / 4 + (u32)u * 32 + lane;
+                    v[u] = j4 * 4 < ne ? l4[j4] : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+#pragma unroll
+                    for (int w = 0; w < 4; w++) {
+                        const u32 j = jb + ((u32)u * 32 + lane) * 4 + w;
+                        if (j >= ne) continue;
+                        const u32 e = w == 0 ? v[u].x : (w == 1 ? v[u].y : (w == 2 ? v[u].z : v[u].w));
+                        const u32 Q = e & 0xFFFFFu;
+                        const u32 sv = slot_entry(Q, j, mod3(e >> 20));
+                        u32 h = store_hash(Q, B.ns_log2);
+                        while (atomicCAS(&tab[h], 0u, sv) != 0u) h = (h + 1) & mask;
+                    }
+                }
             }
             __syncwarp();
             uint4 *dst = reinterpret_cast<uint4 *>(o.tables + ((u64)idx << B.ns_log2));
