@@ -4,6 +4,8 @@ import paper_2507_06579_b200 as eis
 eis.init(0)
 mode = sys.argv[1] if len(sys.argv) > 1 else "bsgs"
 eis.set_option("mode", {"half": eis.MODE_HALF, "bsgs": eis.MODE_BSGS}[mode])
+if os.environ.get("EIS_ALPHA_X16"):
+    eis.set_option("alpha_x16", int(os.environ["EIS_ALPHA_X16"]))
 lo = int(float(sys.argv[2])) if len(sys.argv) > 2 else 9_990_000_000
 hi = int(float(sys.argv[3])) if len(sys.argv) > 3 else 10_000_000_000
 for _ in range(2):
