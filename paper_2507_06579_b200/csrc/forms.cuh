@@ -384,7 +384,7 @@ struct CompD {
 };
 
 EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, double w2, float L,
-                     CompD &o, u32 *err) {
+                     CompD &o, u32 *err, u32 wmask) {
     if (w1 < w2) {
         double t;
         t = u1; u1 = u2; u2 = t;
@@ -395,6 +395,7 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     const double m = v2 - s;
     float fb;
     const float F = fxgcd_x((float)u2, (float)u1, fb);   // b u2 = F (mod u1)
+    warp_reconverge(wmask);
     double G = 1.0, By = u1, Cy = u2, Dy = s, rBy;
     float fbx0;
     if (F == 1.f) {                            // gcd(u1, u2) = 1: G = 1, Bx = m b
@@ -439,6 +440,7 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
         z++;
     }
     if (z & 1) { fby = -fby; fy = -fy; }
+    warp_reconverge(wmask);
     const double bx = fbx, by = fby, x = fx, y = fy;
     if (z != 0) {
         const double cx = dexact_div(fma(Cy, bx, -m * x), By, rBy, err);
@@ -474,11 +476,15 @@ struct GiantComp {
 };
 
 EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, i64 L,
-                               float sqrtd_f, int plain_th, u32 *err) {
+                               float sqrtd_f, int plain_th, u32 *err, u32 wmask) {
     GiantComp r;
     const i64 Q1 = m1.Q, P1 = m1.P;
     if (P2 >= Q2) P2 -= Q2 * (i64)ffloor_div_pos((float)P2, (float)Q2);   // Alg. 4 l.739
-    if (Q1 <= plain_th || Q2 <= plain_th || (Q1 == Q2 && P1 == P2)) {
+    const bool rare = Q1 <= plain_th || Q2 <= plain_th || (Q1 == Q2 && P1 == P2);
+    // lanes of `wmask` that run the NUCOMP fast path (its reconvergence points
+    // must be reached by exactly these lanes)
+    const u32 fmask = warp_ballot(wmask, !rare);
+    if (rare) {
         const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
         r.Q = c.Q;
         r.P = s - floor_mod(s - c.P, c.Q);
@@ -491,7 +497,7 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     const double w2 = rint(((double)P2 * (double)P2 - dd) * rcp64(2.0 * (double)Q2));   // exact
     CompD o;
     if (!nucomp_d((double)(Q1 >> 1), -(double)P1, (double)m1.w, (double)(Q2 >> 1), -(double)P2,
-                  w2, (float)L, o, err)) {
+                  w2, (float)L, o, err, fmask)) {
         const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
         r.Q = c.Q;
         r.P = s - floor_mod(s - c.P, c.Q);

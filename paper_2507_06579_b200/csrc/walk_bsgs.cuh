@@ -305,12 +305,13 @@ struct GiantInfo {
 
 // Advance: mu'_k = rho-reduce(NUCOMPchoose(mu_1, mu'_{k-1})) with its residue and
 // distance; no lookup.  *err counts invariant violations.
-EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err) {
+EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmask = 0xffffffffu) {
     GiantInfo gi;
     const i64 d = (i64)g.d;
     const i64 s = g.s;
     const GiantComp c = giant_compose(g.m1, (i64)g.Qc, (i64)g.Pc, d, s, g.L, (float)g.sqrtd,
-                                      B.plain_th, err);
+                                      B.plain_th, err, wmask);
+    warp_reconverge(wmask);
     gi.kind = c.kind;
     u32 t = mod3(g.t1 + g.tc + 3u - c.tg);       // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
     float dist = g.dist1 + g.distc - c.lg;
@@ -340,6 +341,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err) {
         Q = (i64)Qd;
         P = (i64)Pd;
     }
+    warp_reconverge(wmask);
     gi.nred = nred;
     g.k++;
     g.Qc = (u32)Q;
@@ -604,12 +606,13 @@ bsgs_build_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         // lookup of mu'_2 is left to the giant kernel's pipelined probe
         bool push = false;
         u32 gidx = 0;
+        const u32 kmask = __ballot_sync(FULL_MASK, lane < (int)cnt);
         if (lane < (int)cnt) {
             gidx = myq;
             const BabyRec br = o.brecs[gidx];
             GiantLane g;
             giant_init(g, B, cand_d(a.i0 + (br.off & ~PRIME_BIT)), br, &err);
-            const GiantInfo gi = giant_advance(g, B, &err);
+            const GiantInfo gi = giant_advance(g, B, &err, kmask);
             giant++;
             red += gi.nred;
             o.grecs[gidx] = giant_pack(g, br.off);
@@ -663,17 +666,20 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             }
         }
         if (__all_sync(FULL_MASK, exhausted && g.phase == PH_IDLE)) break;
+        const u32 gmask = __ballot_sync(FULL_MASK, g.phase == PH_GIANT);
         if (g.phase == PH_GIANT) {
             // software pipeline: probe mu'_k (refills start with mu'_2, not yet
             // probed) while computing mu'_{k+1}
             const u32 pQ = g.Qc, pP = g.Pc, pt = g.tc;
             const float pdist = g.distc;
             const Probe pr = store_probe(tab, B.ns_log2, pQ);
-            const GiantInfo gi = giant_advance(g, B, &err);
+            const GiantInfo gi = giant_advance(g, B, &err, gmask);
             giant++;
             red += gi.nred;
             u32 te, j;
-            if (store_resolve(tab, list, B.ns_log2, pr, g.d, pQ, pP, te, j)) {
+            const bool hit = store_resolve(tab, list, B.ns_log2, pr, g.d, pQ, pP, te, j);
+            warp_reconverge(gmask);
+            if (hit) {
                 g.phase = giant_hit(g, te, pt, pdist, g.res) ? PH_DONE : PH_HALF;
             } else if (g.k > g.kcap) {
                 g.phase = PH_HALF;
