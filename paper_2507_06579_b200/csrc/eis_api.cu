@@ -63,6 +63,7 @@ struct Ctx {
     int threads = 256;
     int giant_ctas = 0;
     int half_ksteps = 0;             // 0: chosen per segment from d
+    int two_sided = 1;               // BSGS: two-sided window (R35); 0 = paper's Alg. 1
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
@@ -200,6 +201,12 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), g.alpha_x16 / 16.0f);
         seg_cap = std::min<u64>(SEG, std::max<u64>((12ull << 30) / per, 1ull << 16));
     }
+    // equal segments: a short remainder segment would be all giant-kernel tail
+    {
+        const u64 total = i_last - i_first + 1;
+        const u64 nseg = (total + seg_cap - 1) / seg_cap;
+        seg_cap = (total + nseg - 1) / nseg;
+    }
     CUDA_TRY(cudaEventRecord(g.ev[2], s));
     int iseg = 0;
     bool used_aux = false;
@@ -261,7 +268,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         if (bsgs) {
             BsgsPlan pl;
             CUDA_TRY(cudaStreamSynchronize(g.aux));     // scratch may be (re)allocated below
-            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.giant_ctas, bf.bsgs,
+            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.giant_ctas, g.two_sided, bf.bsgs,
                                   bf.ctr + 2);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
@@ -442,6 +449,7 @@ void eis_finalize(void) {
     fresh.blocks_per_sm = g.blocks_per_sm;
     fresh.giant_ctas = g.giant_ctas;
     fresh.half_ksteps = g.half_ksteps;
+    fresh.two_sided = g.two_sided;
     g = fresh;
 }
 
@@ -472,6 +480,9 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "blocks_per_sm") {
         if (v < 1 || v > 32) return fail(EIS_EINVAL, "blocks_per_sm must be in [1, 32]");
         g.blocks_per_sm = (int)v;
+    } else if (k == "two_sided") {
+        if (v != 0 && v != 1) return fail(EIS_EINVAL, "two_sided must be 0 or 1");
+        g.two_sided = (int)v;
     } else {
         return fail(EIS_EINVAL, "unknown option '%s'", key);
     }
@@ -488,6 +499,7 @@ int64_t eis_get_option(const char *key) {
     if (k == "blocks_per_sm") return g.blocks_per_sm;
     if (k == "giant_ctas") return g.giant_ctas;
     if (k == "half_ksteps") return g.half_ksteps;
+    if (k == "two_sided") return g.two_sided;
     return fail(EIS_EINVAL, "unknown option '%s'", key);
 }
 

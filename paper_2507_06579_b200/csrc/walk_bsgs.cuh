@@ -49,9 +49,27 @@ struct BsgsArgs {
     float alpha;        // baby window factor: W = alpha d^(1/4)
     int plain_th;       // Alg. 4 plain-product threshold on Q (paper: 50)
     float giant_cap_mul;// giant-step cap = giant_cap_mul * (d^(1/4) + 10)
+    int two_sided;      // R35: conjugate hits + doubled stride (0 = the paper's one-sided Alg. 1)
 };
 
 EIS_HD u32 mod3(u32 v) { return v % 3u; }
+
+// Two-sided window (R35).  Conjugation reverses the principal cycle
+// (R13: a_{j+1} = conj(a_j) when Q_j = Q_{j-1}), so the conjugates of the stored
+// ideals theta_1..theta_n are the n cycle ideals just before a_p = O: the store
+// covers the arc of distances [R - dist_last + O(log sqrt d), R + dist_last]
+// around every multiple of R.  A giant ideal mu = (alpha) whose conjugate is the
+// stored theta_j = (beta) gives conj(alpha) = +-eps^-1 beta, so t(eps) = t(mu) +
+// t(theta_j) (t(conj x) = -t(x), R13); a direct match gives t(mu) - t(theta_j).
+// Both are read from one probe (same Q, P or -P mod Q).  The arc is ~2 dist_last
+// long, so the giant stride may be mu_1^2 with mu_1 a margin M below the window
+// end: stride 2 dist_1 + kappa <= 2 dist_last - 2M + kappa stays shorter than the
+// arc while 2M >= kappa_2 + kappa_k + log sqrt d + (largest rho-step distance),
+// kappa being the composition excess (< 2 log sqrt d; <= 16.4 nats seen at 1e11,
+// SURVEY.md 8(c) #14).  M = 2 ln d + 4 nats (= 4 log sqrt d + 4) is used.
+EIS_HD float two_sided_margin2(u64 d) {            // M in log2 units
+    return 2.f * log2_approx((float)d) + 4.f / LN2F;
+}
 
 // ---------------------------------------------------------------- the store --
 EIS_HD u32 list_entry(u32 Q, u32 traw) { return Q | (traw << 20); }
@@ -89,9 +107,31 @@ EIS_HD Probe store_probe(const u32 *tab, int ns_log2, u32 Q) {
     return p;
 }
 
-// true on a hit: t3 = t(theta) mod 3, j = the entry index
-EIS_HD bool store_resolve(const u32 *tab, const u32 *list, int ns_log2, Probe p, u64 d, u32 Q,
-                          u32 P, u32 &t3, u32 &j) {
+// Hit kinds of a lookup of the reduced (Q, P): the stored ideal is (Q, P) itself
+// or its conjugate (Q, -P mod Q) (R35).
+enum HitKind : int { HIT_NONE = 0, HIT_DIRECT = 1, HIT_CONJ = 2 };
+
+// P-bar: the canonical representative in (s - Q, s] of -P mod Q
+EIS_HD u32 conj_P(u32 Q, u32 P, u32 s) {
+    const u32 r = (s + P) % Q;
+    return s - r;
+}
+
+// Entry jj >= 1 holds (Q_j, P_j) with P_j^2 = d - Q_{j-1} Q_j, P_j > 0 on reduced
+// ideals, so Q_{j-1} identifies P_j; entry 0 is (2, P_1) = O, the only reduced
+// ideal with Q = 2 (self-conjugate).
+EIS_HD int match_kind(u64 d, u32 Q, u32 P, u32 s, u32 jj, u32 Qprev) {
+    if (jj == 0) return HIT_DIRECT;
+    const u64 nrm = d - (u64)Qprev * Q;
+    if ((u64)P * P == nrm) return HIT_DIRECT;
+    const u32 Pb = conj_P(Q, P, s);
+    if ((u64)Pb * Pb == nrm) return HIT_CONJ;
+    return HIT_NONE;
+}
+
+// Resolve a probe of (Q, P): the hit kind, t3 = t(theta) mod 3, j = the entry.
+EIS_HD int store_resolve(const u32 *tab, const u32 *list, int ns_log2, Probe p, u64 d, u32 s,
+                         u32 Q, u32 P, u32 &t3, u32 &j) {
     const u32 mask = (1u << ns_log2) - 1;
     const u32 qk = Q >> 2;
     u32 h = p.h;
@@ -102,19 +142,15 @@ EIS_HD bool store_resolve(const u32 *tab, const u32 *list, int ns_log2, Probe p,
         for (u32 i = 0; i < 4; i++) {
             const u32 e = i == 0 ? g.x : (i == 1 ? g.y : (i == 2 ? g.z : g.w));
             if (i < i0) continue;
-            if (e == 0) return false;
+            if (e == 0) return HIT_NONE;
             if ((e & 0x3FFFFu) == qk) {
                 const u32 jj = ((e >> 18) & 0x7FFu) - 1;
-                // entry 0 is (2, P_1), the only reduced ideal with Q = 2
-                bool hit = (jj == 0);
-                if (!hit) {
-                    const u64 Qp = list[jj - 1] & 0xFFFFFu;   // Q_{j-1}
-                    hit = (u64)P * P == d - Qp * Q;            // P_j^2 = d - Q_{j-1} Q_j
-                }
-                if (hit) {
+                const u32 Qprev = jj ? (list[jj - 1] & 0xFFFFFu) : 0u;
+                const int k = match_kind(d, Q, P, s, jj, Qprev);
+                if (k != HIT_NONE) {
                     t3 = e >> 29;
                     j = jj;
-                    return true;
+                    return k;
                 }
             }
         }
@@ -134,7 +170,8 @@ struct BabyLane {
     u32 n;              // list entries (those of the last partial group are pending)
     u32 pe0, pe1, pe2;  // pending entries of the group [n & ~3, n), not yet in memory
     int extras;         // -1 before the window is complete, then 2, 1
-    u32 Q1, P1, t1;     // mu_1
+    float M2;           // two-sided margin (log2 units), 0 = one-sided
+    u32 Q1, P1, t1;     // mu_1 (Q1 = 0: not chosen yet)
     float dist1;
     u32 phase, res;
 };
@@ -188,13 +225,16 @@ EIS_HD bool bsgs_begin(BabyLane &ln, u32 *list, const BsgsArgs &B, u64 d) {
     ln.n = 2;
     ln.extras = -1;
     ln.phase = PH_BABY;
-    if (ln.dist >= ln.W2) {                 // window already complete at theta_2
+    ln.M2 = two_sided_margin2(d);
+    if (!B.two_sided || ln.W2 < 3.f * ln.M2) ln.M2 = 0.f;   // one-sided (paper's Alg. 1)
+    ln.Q1 = 0;
+    if (ln.dist >= ln.W2 - ln.M2) {         // mu_1 = theta_2
         ln.Q1 = b.Q;
         ln.P1 = b.P;
         ln.t1 = mod3(b.t2 >> 1);
         ln.dist1 = ln.dist;
-        ln.extras = 2;
     }
+    if (ln.dist >= ln.W2) ln.extras = 2;    // window already complete at theta_2
     return false;
 }
 
@@ -234,13 +274,14 @@ EIS_HD int bsgs_baby(BabyLane &ln, u32 *list, const BsgsArgs &B, int kmax) {
             return k;
         }
         if (ln.extras < 0) {
-            if (ln.dist >= ln.W2 || (int)ln.n >= B.cap - 2) {
+            const bool end = ln.dist >= ln.W2 || (int)ln.n >= B.cap - 2;
+            if (ln.Q1 == 0 && (end || ln.dist >= ln.W2 - ln.M2)) {
                 ln.Q1 = f_to_u(ln.st.Q);                 // mu_1 = theta_j (just stored)
                 ln.P1 = f2u_bits(ln.st.Pm) - 0x4B000000u;
                 ln.t1 = mod3(ln.st.t2 >> 1);
                 ln.dist1 = ln.dist;
-                ln.extras = 2;                           // "Compute two more ideals" (l.560)
             }
+            if (end) ln.extras = 2;                      // "Compute two more ideals" (l.560)
         } else if (--ln.extras == 0) {
             if ((ln.n & 3u) != 0) list_flush(list, ln.n, e0, e1, e2, e3);
             ln.phase = PH_GIANT;
@@ -354,27 +395,52 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
 // Verdict for a store hit on mu'_k = (t, dist) (R14):
 // 1 = accepted, result in res (eps = mu'_k / theta); 0 = inconclusive guard
 // (caller switches the d to the exact half walk).
-EIS_HD int giant_hit(const GiantLane &g, u32 te, u32 t, float dist, u32 &res) {
-    if (dist - g.dist_last >= GUARD_LOG2) {
+// A conjugate hit of mu = (Q, P) is the relation eps^-m = conj(alpha)/beta with
+// m R = dist + log theta_j - log N(mu) >= dist - log(Q/2) (R35): it is
+// nontrivial once dist - log2(Q/2) >= the guard.
+EIS_HD int giant_hit(const GiantLane &g, int kind, u32 te, u32 t, float dist, u32 Q, u32 &res) {
+    if (kind == HIT_CONJ) {
+        if (dist - log2_approx(0.5f * (float)Q) >= GUARD_LOG2) {
+            res = mod3(t + te);
+            return 1;
+        }
+    } else if (dist - g.dist_last >= GUARD_LOG2) {
         res = mod3(t + 3u - te);
         return 1;
     }
     return 0;
 }
 
-// One unpipelined giant step (advance + lookup), used by the CPU emulation.
-// Sets PH_DONE on an accepted hit, PH_HALF on an inconclusive guard or past the cap.
-EIS_HD GiantInfo bsgs_giant(GiantLane &g, const u32 *tab, const u32 *list, const BsgsArgs &B,
-                            u32 *err) {
-    const GiantInfo gi = giant_advance(g, B, err);
-    u32 te, j;
-    if (store_resolve(tab, list, B.ns_log2, store_probe(tab, B.ns_log2, g.Qc), g.d, g.Qc, g.Pc,
-                      te, j)) {
-        g.phase = giant_hit(g, te, g.tc, g.distc, g.res) ? PH_DONE : PH_HALF;
-        return gi;
+// k = 2: mu'_2 = rho-reduce(mu_1 * mu_1) (NUDUPL).  With the two-sided window
+// (R35) and enough margin, mu'_2 becomes the giant stride: mu''_1 = mu'_2 and
+// mu''_k = mu'_2 * mu''_{k-1}.  Same lane mask rules as giant_advance.
+EIS_HD GiantInfo giant_start(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmask = 0xffffffffu) {
+    const GiantInfo gi = giant_advance(g, B, err, wmask);
+    const float M2 = two_sided_margin2(g.d);
+    if (B.two_sided && g.dist1 >= 2.f * M2 && g.dist_last - g.dist1 >= M2) {
+        g.m1 = mu1_form((i64)g.Qc, (i64)g.Pc, (i64)g.d, err);
+        g.t1 = g.tc;
+        g.dist1 = g.distc;
     }
-    if (g.k > g.kcap) g.phase = PH_HALF;
     return gi;
+}
+
+// Unpipelined lookup of the current giant ideal (CPU emulation).  Sets PH_DONE
+// on an accepted hit, PH_HALF on an inconclusive guard or past the cap; returns
+// true when the d is decided.
+EIS_HD bool giant_lookup(GiantLane &g, const u32 *tab, const u32 *list, const BsgsArgs &B) {
+    u32 te, j;
+    const int kind = store_resolve(tab, list, B.ns_log2, store_probe(tab, B.ns_log2, g.Qc), g.d,
+                                   (u32)g.s, g.Qc, g.Pc, te, j);
+    if (kind != HIT_NONE) {
+        g.phase = giant_hit(g, kind, te, g.tc, g.distc, g.Qc, g.res) ? PH_DONE : PH_HALF;
+        return true;
+    }
+    if (g.k > g.kcap) {
+        g.phase = PH_HALF;
+        return true;
+    }
+    return false;
 }
 
 // Everything the giant kernel needs to resume a d (written by the build kernel
@@ -612,7 +678,7 @@ bsgs_build_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             const BabyRec br = o.brecs[gidx];
             GiantLane g;
             giant_init(g, B, cand_d(a.i0 + (br.off & ~PRIME_BIT)), br, &err);
-            const GiantInfo gi = giant_advance(g, B, &err, kmask);
+            const GiantInfo gi = giant_start(g, B, &err, kmask);
             giant++;
             red += gi.nred;
             o.grecs[gidx] = giant_pack(g, br.off);
@@ -677,10 +743,10 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             giant++;
             red += gi.nred;
             u32 te, j;
-            const bool hit = store_resolve(tab, list, B.ns_log2, pr, g.d, pQ, pP, te, j);
+            const int kind = store_resolve(tab, list, B.ns_log2, pr, g.d, (u32)g.s, pQ, pP, te, j);
             warp_reconverge(gmask);
-            if (hit) {
-                g.phase = giant_hit(g, te, pt, pdist, g.res) ? PH_DONE : PH_HALF;
+            if (kind != HIT_NONE) {
+                g.phase = giant_hit(g, kind, te, pt, pdist, pQ, g.res) ? PH_DONE : PH_HALF;
             } else if (g.k > g.kcap) {
                 g.phase = PH_HALF;
             }
@@ -772,8 +838,9 @@ inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha) {
 // Size one segment buffer (seg_len candidates bound the survivors) and choose
 // the launch shapes.  ctr: 4 device counters (zeroed by bsgs_launch_baby).
 inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
-                        int giant_ctas, BsgsScratch &scr, u32 *ctr) {
+                        int giant_ctas, int two_sided, BsgsScratch &scr, u32 *ctr) {
     BsgsArgs &B = pl.B;
+    B.two_sided = two_sided;
     B.alpha = alpha_x16 / 16.0f;
     const BsgsSizes z = bsgs_sizes(d_hi, B.alpha);
     B.ns_log2 = z.ns_log2;

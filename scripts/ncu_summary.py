@@ -32,6 +32,9 @@ for r in rows[2:]:
         lines.append(f"  {n.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):30s} {v:8.3f}")
     lines.append("")
 # launch list
+import os
+if not os.path.exists(launches):
+    open(out, "w").write("\n".join(lines) + "\n"); print("\n".join(lines)); sys.exit(0)
 lr = list(csv.reader(open(launches)))
 hi = [i for i, r in enumerate(lr) if r and r[0] == "ID"][0]
 H = lr[hi]

@@ -3,7 +3,7 @@
 // CPU, one d at a time, so their arithmetic can be checked against the oracle
 // without a GPU.  Not part of the product library.
 //
-// usage: kernel_emu MODE ALPHA_X16 NS_LOG2 < d-list     (MODE: half | bsgs)
+// usage: kernel_emu MODE ALPHA_X16 NS_LOG2 [PLAIN_TH [TWO_SIDED]] < d-list  (MODE: half | bsgs)
 // prints per d: "d t baby giant reduce fallback err kinds(plain,comp,dupl)"
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +24,7 @@ int main(int argc, char **argv) {
     const int ns_fixed = atoi(argv[3]);
     B.plain_th = argc > 4 ? atoi(argv[4]) : 50;
     B.giant_cap_mul = 20.0f;
+    B.two_sided = argc > 5 ? atoi(argv[5]) : 1;
     std::vector<u32> bm(1 << 10);
     std::vector<u32> tab(1 << 14), lst(1 << 12);
     unsigned long long d;
@@ -62,8 +63,12 @@ int main(int argc, char **argv) {
                     const BabyRec br = baby_pack(ln, 0);
                     GiantLane g;
                     giant_init(g, B, d, br, &err);
-                    while (g.phase == PH_GIANT) {
-                        GiantInfo gi = bsgs_giant(g, tab.data(), lst.data(), B, &err);
+                    GiantInfo gi = giant_start(g, B, &err);   // k = 2 (build kernel)
+                    giant++;
+                    red += gi.nred;
+                    kinds[gi.kind]++;
+                    while (!giant_lookup(g, tab.data(), lst.data(), B)) {   // giant kernel
+                        gi = giant_advance(g, B, &err);
                         giant++;
                         red += gi.nred;
                         kinds[gi.kind]++;

@@ -30,8 +30,8 @@ def emu(tmp_path_factory):
     return exe
 
 
-def run(exe, ds, mode, alpha_x16=16, ns_log2=0, plain_th=50):
-    out = subprocess.run([exe, mode, str(alpha_x16), str(ns_log2), str(plain_th)],
+def run(exe, ds, mode, alpha_x16=16, ns_log2=0, plain_th=50, two_sided=1):
+    out = subprocess.run([exe, mode, str(alpha_x16), str(ns_log2), str(plain_th), str(two_sided)],
                          input="\n".join(str(int(d)) for d in ds), capture_output=True,
                          text=True, check=True).stdout
     rows = np.array([[int(v) for v in ln.split()] for ln in out.splitlines() if ln.strip()],
@@ -56,12 +56,13 @@ def test_every_d_upto_2e5(emu, mode):
     assert rows[:, 6].sum() == 0 and rows[:, 5].sum() == 0     # no invariant errors / fallbacks
 
 
+@pytest.mark.parametrize("two_sided", [1, 0])
 @pytest.mark.parametrize("scale", [10**7, 10**8, 10**9, 10**10, 10**11])
-def test_bsgs_samples_at_scale(emu, scale):
+def test_bsgs_samples_at_scale(emu, scale, two_sided):
     s = workloads.sample_candidates(scale - 10**6, scale, 120, seed=scale % 1000 + 3)
     s = np.array([d for d in s if c_oracle.is_squarefree(int(d))], dtype=np.uint64)
     want = c_oracle.classify_list(s)
-    rows = run(emu, s, "bsgs")
+    rows = run(emu, s, "bsgs", two_sided=two_sided)
     assert np.array_equal(rows[:, 1], want)
     assert rows[:, 6].sum() == 0 and rows[:, 5].sum() == 0
     assert rows[:, 3].sum() > 0                                  # giant steps were taken
@@ -75,6 +76,21 @@ def test_bsgs_results_independent_of_alpha_and_threshold(emu, alpha_x16, plain_t
     rows = run(emu, ds, "bsgs", alpha_x16=alpha_x16, plain_th=plain_th)
     assert np.array_equal(rows[:, 1], want)
     assert rows[:, 6].sum() == 0
+
+
+def test_two_sided_window_halves_giant_steps(emu):
+    """DESIGN.md R35: with conjugate matches the store covers an arc of ~2W
+    around each multiple of R, so the stride mu_1^2 (~2W - 2M) is safe and the
+    giant-step count drops by ~1.7x at 1e10; every t is unchanged, including
+    those decided by a conjugate hit."""
+    s = workloads.sample_candidates(10**10 - 10**7, 10**10, 400, seed=35)
+    s = np.array([d for d in s if c_oracle.is_squarefree(int(d))], dtype=np.uint64)
+    want = c_oracle.classify_list(s)
+    one = run(emu, s, "bsgs", alpha_x16=24, two_sided=0)
+    two = run(emu, s, "bsgs", alpha_x16=24, two_sided=1)
+    assert np.array_equal(one[:, 1], want) and np.array_equal(two[:, 1], want)
+    assert two[:, 5].sum() == 0 and two[:, 6].sum() == 0
+    assert one[:, 3].sum() > 1.5 * two[:, 3].sum()
 
 
 def test_verbatim_guard_case_661(emu):
