@@ -198,7 +198,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     const bool bsgs = want_bsgs(cand_d(i_first));
     u64 seg_cap = SEG;
     if (bsgs) {
-        const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), g.alpha_x16 / 16.0f);
+        const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), g.alpha_x16 / 16.0f, g.two_sided);
         seg_cap = std::min<u64>(SEG, std::max<u64>((12ull << 30) / per, 1ull << 16));
     }
     // equal segments: a short remainder segment would be all giant-kernel tail

@@ -335,7 +335,7 @@ EIS_HD Mu1Form mu1_form(i64 Q1, i64 P1, i64 d, u32 *err) {
 
 // Algorithm 4 NUCOMPchoose for reduced ideals
 // I1 = mu_1 = [Q1/2, (P1+sqrt d)/2] (pre-normalised) and I2 = [Q2/2, (P2+sqrt d)/2].
-EIS_HD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 L, double sqrtd,
+EIS_HD_COLD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 L, double sqrtd,
                               int plain_th, u32 *err) {
     const i64 Q1 = m1.Q, P1 = m1.P;
     P2 = P2 < Q2 ? P2 : floor_mod(P2, Q2);

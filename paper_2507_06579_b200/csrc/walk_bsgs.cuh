@@ -1,34 +1,43 @@
 // walk_bsgs.cuh -- K3 in BSGS mode: the paper's Algorithm 1
 // with residues in Z/3 (l.585-603): baby steps rho into a per-d store, then
 // giant steps mu_k = mu_1 * mu'_{k-1} by NUCOMPchoose (forms.cuh), rho-reduction,
-// and a store lookup.
+// and a store lookup; with the two-sided window of DESIGN.md R35.
 //
 // Three kernels per segment (K3 BSGS):
-//   bsgs_baby_kernel   persistent lanes, per-lane refill: bsgs_begin + baby steps in
-//                      the half walk's exact FP32 form, each entry APPENDED to a dense
-//                      per-d list (sequential writes: full sectors, no L2 capacity
-//                      limit).  Symmetry exits (l.553-556) finish the d; completed
-//                      windows are queued for the build kernel.
-//   bsgs_build_kernel  one warp per 32 queued d: each store is built as a hash table
-//                      in shared memory from the list and written out with coalesced
-//                      full-line stores; then the 32 lanes take the k = 2 giant step
-//                      (always NUDUPL, Alg. 4 l.745) together and queue the d for
-//   bsgs_giant_kernel  persistent lanes with per-lane refill (giant counts are
-//                      heavy-tailed) and a software-pipelined lookup.
+//   bsgs_window_kernel  one warp per wave of 32 survivors, in lockstep: every lane
+//                       takes the same number nw of baby steps (the window is
+//                       nw entries, ~ alpha d^(1/4) nats; R6/R29: only step
+//                       counts depend on it), so the loop has no per-lane exit
+//                       test besides the symmetry exit (l.553-556).  Entries are
+//                       kept in registers in blocks of 8 (indices known at
+//                       compile time) and written as two 16-byte stores per lane
+//                       into a dense per-d list.  The same warp then builds the
+//                       32 stores, one d at a time, as bucketed hash tables in
+//                       shared memory from the (L2-resident) lists and writes
+//                       them out with coalesced 16-byte stores.
+//   bsgs_prep_kernel    k = 2 for every windowed d in lockstep (mu'_2 = mu_1^2,
+//                       NUDUPL, Alg. 4 l.745; R35 may make it the stride).
+//   bsgs_giant_kernel   persistent lanes with per-lane refill (giant counts are
+//                       heavy-tailed) and a software-pipelined lookup.
 //
 // The store ("dictionary of ideals", l.549, l.607).  list[j] = Q_j | t_j << 20 for
-// the j-th baby entry (theta_{j+1} <-> (Q_j, P_j); t unreduced, < 2^12); the
-// table maps Q to j: slot = (Q >> 2) | (j + 1) << 18 | (t_j mod 3) << 29, 0 =
-// empty.  P is not stored: on the principal cycle P_j^2 = d - Q_{j-1} Q_j with
-// P_j > 0 (rho), so a reduced (Q*, P*) matches entry j >= 1 iff Q* = Q_j and
-// P*^2 = d - Q_{j-1} Q* (exact, u64); entry 0 is (2, P_1), the only reduced
-// ideal of norm 1 (R34).  The paper's Bloom filter plays the table's
-// role (no false negatives; positives verified exactly).
+// the j-th baby entry (theta_{j+1} <-> (Q_j, P_j); t unreduced, < 2^12).  The
+// table is nb buckets of BKT = 16 slots (64 bytes, two DRAM sectors); slot =
+// (Q >> 2) | (j + 1) << 18 | (t_j mod 3) << 29, 0 = empty (Q = 2 mod 4 on
+// reduced ideals, so Q >> 2 identifies Q).  An entry goes to the first free
+// slot of bucket h(Q), else of the following buckets; slots fill in order, so
+// a lookup stops at the first empty slot.  P is not stored: on the principal
+// cycle P_j^2 = d - Q_{j-1} Q_j with P_j > 0 (rho), so a reduced (Q*, P*)
+// matches entry j >= 1 iff Q* = Q_j and P*^2 = d - Q_{j-1} Q* (exact, u64);
+// entry 0 is (2, P_1), the only reduced ideal of norm 1 (R34).  The
+// paper's Bloom filter plays the table's role (no false negatives; positives
+// verified exactly).
 //
-// The guard (R14): a hit counts if log mu'_k - log theta >= 1.  With
-// log theta <= the distance of the last stored entry, a hit with log mu'_k -
-// dist_last >= 1 always passes; any other hit (only possible for tiny d, where
-// mu'_2 can land inside the window) sends the d to the exact half walk.
+// The guard (R14, R32): a direct hit counts if log mu'_k - log theta
+// >= 1.  With log theta <= the distance of the last stored entry, a hit with
+// log mu'_k - dist_last >= 1 always passes; any other hit (only possible for
+// tiny d, where mu'_2 can land inside the window) sends the d to the exact half
+// walk.  Conjugate hits: R35.
 //
 // Per-lane state machines are __host__ __device__ and are run by the CPU
 // emulation harness tests/emu/kernel_emu.cu.
@@ -39,20 +48,23 @@
 
 constexpr float LN2F = 0.69314718f;
 constexpr float GUARD_LOG2 = 1.0f / LN2F;    // "log mu'_k - log theta >= 1" in log2 units
+constexpr int BKT = 16;                       // slots per table bucket (64 bytes)
+constexpr float BKT_LOAD = 0.62f;             // table load factor
 
 enum LanePhase : u32 { PH_IDLE = 0, PH_BABY = 1, PH_GIANT = 2, PH_HALF = 3, PH_DONE = 4 };
 
 struct BsgsArgs {
-    int ns_log2;        // table slots per d = 1 << ns_log2
-    int cap;            // max list entries per d (<= 2040)
-    int lcap;           // list stride per d (>= cap, multiple of 32)
-    float alpha;        // baby window factor: W = alpha d^(1/4)
+    int nw;             // window entries per d (multiple of 8, <= 2040)
+    int j1;             // entry index of mu_1 (= 7 mod 8: the end of a block)
+    int nb;             // table buckets per d
+    int lcap;           // list stride per d (>= nw, multiple of 32)
     int plain_th;       // Alg. 4 plain-product threshold on Q (paper: 50)
     float giant_cap_mul;// giant-step cap = giant_cap_mul * (d^(1/4) + 10)
     int two_sided;      // R35: conjugate hits + doubled stride (0 = the paper's one-sided Alg. 1)
 };
 
 EIS_HD u32 mod3(u32 v) { return v % 3u; }
+EIS_HD u32 mod3_small(u32 v) { return v - 3u * ((v * 0x5556u) >> 16); }   // v < 2^15
 
 // Two-sided window (R35).  Conjugation reverses the principal cycle
 // (R13: a_{j+1} = conj(a_j) when Q_j = Q_{j-1}), so the conjugates of the stored
@@ -74,36 +86,48 @@ EIS_HD float two_sided_margin2(u64 d) {            // M in log2 units
 // ---------------------------------------------------------------- the store --
 EIS_HD u32 list_entry(u32 Q, u32 traw) { return Q | (traw << 20); }
 EIS_HD u32 slot_entry(u32 Q, u32 j, u32 t3) { return (Q >> 2) | ((j + 1) << 18) | (t3 << 29); }
-EIS_HD u32 store_hash(u32 Q, int ns_log2) { return (Q * 0x9E3779B1u) >> (32 - ns_log2); }
+EIS_HD u32 slot_of(u32 e, u32 j) { return slot_entry(e & 0xFFFFFu, j, mod3_small(e >> 20)); }
+EIS_HD u32 store_bucket(u32 Q, u32 nb) {           // multiply-shift hash onto [0, nb)
+    return (u32)(((u64)(Q * 0x9E3779B1u) * nb) >> 32);
+}
+EIS_HD u32 next_bucket(u32 b, u32 nb) { return b + 1 == nb ? 0u : b + 1; }
 
-// host/emulation build: sequential linear probing into a zeroed table
-EIS_HD void store_build_seq(u32 *tab, int ns_log2, const u32 *list, u32 n) {
-    const u32 mask = (1u << ns_log2) - 1;
+// host/emulation build: sequential insertion into a zeroed table
+EIS_HD void store_build_seq(u32 *tab, u32 nb, const u32 *list, u32 n) {
     for (u32 j = 0; j < n; j++) {
         const u32 e = list[j], Q = e & 0xFFFFFu;
-        u32 h = store_hash(Q, ns_log2);
-        while (tab[h] != 0) h = (h + 1) & mask;
-        tab[h] = slot_entry(Q, j, mod3(e >> 20));
+        u32 b = store_bucket(Q, nb);
+        for (;;) {
+            u32 i = 0;
+            while (i < (u32)BKT && tab[b * BKT + i] != 0) i++;
+            if (i < (u32)BKT) {
+                tab[b * BKT + i] = slot_of(e, j);
+                break;
+            }
+            b = next_bucket(b, nb);
+        }
     }
 }
 
-// Lookup of a reduced (Q, P) (P canonical): tables are zero-filled, so linear
-// probing stops at the first empty slot; slots are read four at a time (one
-// 16-byte load per aligned group).  Split so the giant kernel can issue the
-// first group load, compute the next giant step, then resolve.
+// Lookup of a reduced (Q, P) (P canonical).  Split so the giant kernel can issue
+// the bucket load, compute the next giant step, then resolve.
 struct Probe {
-    u32 h;
-    uint4 grp;
+    u32 b;
+    uint4 g0, g1, g2, g3;
 };
 
-EIS_HD uint4 load_group(const u32 *tab, u32 h) {
-    return *reinterpret_cast<const uint4 *>(tab + (h & ~3u));
+EIS_HD void load_bucket(const u32 *tab, u32 b, Probe &p) {
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tab + (size_t)b * BKT);
+    p.b = b;
+    p.g0 = t4[0];
+    p.g1 = t4[1];
+    p.g2 = t4[2];
+    p.g3 = t4[3];
 }
 
-EIS_HD Probe store_probe(const u32 *tab, int ns_log2, u32 Q) {
+EIS_HD Probe store_probe(const u32 *tab, u32 nb, u32 Q) {
     Probe p;
-    p.h = store_hash(Q, ns_log2);
-    p.grp = load_group(tab, p.h);
+    load_bucket(tab, store_bucket(Q, nb), p);
     return p;
 }
 
@@ -129,61 +153,48 @@ EIS_HD int match_kind(u64 d, u32 Q, u32 P, u32 s, u32 jj, u32 Qprev) {
     return HIT_NONE;
 }
 
+EIS_HD u32 bucket_slot(const Probe &p, int i) {      // i: compile-time after unrolling
+    const uint4 &g = i < 4 ? p.g0 : (i < 8 ? p.g1 : (i < 12 ? p.g2 : p.g3));
+    const int k = i & 3;
+    return k == 0 ? g.x : (k == 1 ? g.y : (k == 2 ? g.z : g.w));
+}
+
 // Resolve a probe of (Q, P): the hit kind, t3 = t(theta) mod 3, j = the entry.
-EIS_HD int store_resolve(const u32 *tab, const u32 *list, int ns_log2, Probe p, u64 d, u32 s,
+// The bucket is scanned without branches (key-match and empty-slot masks); a
+// key match (about one per d) re-reads its slot and checks P (R34, R35).
+EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d, u32 s,
                          u32 Q, u32 P, u32 &t3, u32 &j) {
-    const u32 mask = (1u << ns_log2) - 1;
     const u32 qk = Q >> 2;
-    u32 h = p.h;
-    uint4 g = p.grp;
     for (;;) {
-        const u32 i0 = h & 3u;
+        u32 mm = 0, em = 0;
 #pragma unroll
-        for (u32 i = 0; i < 4; i++) {
-            const u32 e = i == 0 ? g.x : (i == 1 ? g.y : (i == 2 ? g.z : g.w));
-            if (i < i0) continue;
-            if (e == 0) return HIT_NONE;
-            if ((e & 0x3FFFFu) == qk) {
-                const u32 jj = ((e >> 18) & 0x7FFu) - 1;
-                const u32 Qprev = jj ? (list[jj - 1] & 0xFFFFFu) : 0u;
-                const int k = match_kind(d, Q, P, s, jj, Qprev);
-                if (k != HIT_NONE) {
-                    t3 = e >> 29;
-                    j = jj;
-                    return k;
-                }
+        for (int i = 0; i < BKT; i++) {
+            const u32 e = bucket_slot(p, i);
+            mm |= (u32)((e & 0x3FFFFu) == qk) << i;
+            em |= (u32)(e == 0) << i;
+        }
+        mm &= (em & (0u - em)) - 1u;                   // slots before the first empty one
+        while (mm) {
+            const int i = __builtin_ctz_portable(mm);
+            mm &= mm - 1;
+            const u32 e = tab[(size_t)p.b * BKT + i];
+            const u32 jj = ((e >> 18) & 0x7FFu) - 1;
+            const u32 Qprev = jj ? (list[jj - 1] & 0xFFFFFu) : 0u;
+            const int k = match_kind(d, Q, P, s, jj, Qprev);
+            if (k != HIT_NONE) {
+                t3 = e >> 29;
+                j = jj;
+                return k;
             }
         }
-        h = ((h | 3u) + 1) & mask;
-        g = load_group(tab, h);
+        if (em) return HIT_NONE;
+        load_bucket(tab, next_bucket(p.b, nb), p);       // bucket full: continue
     }
 }
 
-// ------------------------------------------------------------ baby phase --
+// ----------------------------------------------------------- window phase --
 // Baby steps in the half walk's exact FP32 form (walk_half.cuh) plus the log2
 // distance of each generator multiplier (P_j + sqrt d)/Q_{j-1}.
-struct BabyLane {
-    BabyStateF st;
-    float dist;         // log2 theta_{j+1} of the current ideal
-    float sqd_m;        // sqrt(d) - 2^23 (P + sqrt d = Pm + sqd_m)
-    float W2;           // window in log2 units
-    u32 n;              // list entries (those of the last partial group are pending)
-    u32 pe0, pe1, pe2;  // pending entries of the group [n & ~3, n), not yet in memory
-    int extras;         // -1 before the window is complete, then 2, 1
-    float M2;           // two-sided margin (log2 units), 0 = one-sided
-    u32 Q1, P1, t1;     // mu_1 (Q1 = 0: not chosen yet)
-    float dist1;
-    u32 phase, res;
-};
-
-struct __align__(32) BabyRec {       // baby kernel -> build kernel
-    u32 off;            // survivor-list entry (offset | PRIME_BIT)
-    u32 n;              // list entries
-    u32 Q1, P1, t1;     // mu_1
-    float dist1, dist_last;
-    u32 pad;
-};
-
 EIS_HD bool baby_step_fd(BabyStateF &st, float sqd_m, float &dist) {
     const float num = st.Pm + st.sm;
     const float rq = rcp_approx(st.Q);
@@ -203,106 +214,89 @@ EIS_HD bool baby_step_fd(BabyStateF &st, float sqd_m, float &dist) {
 
 EIS_HD u32 f_to_u(float v) { return f2u_bits(v + 8388608.0f) - 0x4B000000u; }   // v < 2^23
 
-// Start d: entries theta_1 = (2, P_1) and theta_2 = (Q_1, P_1).  True if finished.
-EIS_HD bool bsgs_begin(BabyLane &ln, u32 *list, const BsgsArgs &B, u64 d) {
+
+struct WinLane {
+    BabyStateF st;
+    float dist;         // log2 theta_{j+1} of the current ideal
+    float sqd_m;        // sqrt(d) - 2^23 (P + sqrt d = Pm + sqd_m)
+    u32 Q1, P1, t1;     // mu_1
+    float dist1;
+    u32 res;            // t at the symmetry exit
+    bool live;          // no symmetry exit yet
+};
+
+struct __align__(32) BabyRec {       // window kernel -> prep kernel
+    u32 off;            // survivor-list entry (offset | PRIME_BIT)
+    u32 n;              // list entries
+    u32 Q1, P1, t1;     // mu_1
+    float dist1, dist_last;
+    u32 pad;
+};
+
+// Entries 0 = theta_1 = (2, P_1) and 1 = theta_2 = (Q_1, P_1).  False if the d is
+// already finished (res set).
+EIS_HD bool win_begin(WinLane &w, u64 d, u32 &e0, u32 &e1) {
     BabyState b;
     u32 r1;
-    const bool fin = baby_init(b, d, &r1);
-    if (fin) {
-        ln.res = r1;
-        ln.phase = PH_DONE;
-        return true;
+    w.live = false;
+    if (baby_init(b, d, &r1)) {
+        w.res = r1;
+        return false;
     }
-    ln.st = baby_to_f(b);
+    w.st = baby_to_f(b);
     const float sqd = (float)sqrt((double)d);
-    ln.sqd_m = sqd - 8388608.0f;
-    ln.W2 = B.alpha * sqrtf(sqd) / LN2F;
-    (void)list;
-    ln.pe0 = list_entry(2u, 0u);                      // entries 0 and 1, written with
-    ln.pe1 = list_entry(b.Q, b.t2 >> 1);              // the first full group
-    ln.pe2 = 0;
-    ln.dist = log2_approx(((float)b.P + sqd) * 0.5f);
-    ln.n = 2;
-    ln.extras = -1;
-    ln.phase = PH_BABY;
-    ln.M2 = two_sided_margin2(d);
-    if (!B.two_sided || ln.W2 < 3.f * ln.M2) ln.M2 = 0.f;   // one-sided (paper's Alg. 1)
-    ln.Q1 = 0;
-    if (ln.dist >= ln.W2 - ln.M2) {         // mu_1 = theta_2
-        ln.Q1 = b.Q;
-        ln.P1 = b.P;
-        ln.t1 = mod3(b.t2 >> 1);
-        ln.dist1 = ln.dist;
-    }
-    if (ln.dist >= ln.W2) ln.extras = 2;    // window already complete at theta_2
-    return false;
+    w.sqd_m = sqd - 8388608.0f;
+    e0 = list_entry(2u, 0u);
+    e1 = list_entry(b.Q, b.t2 >> 1);
+    w.dist = log2_approx(((float)b.P + sqd) * 0.5f);
+    w.Q1 = 0;
+    w.live = true;
+    return true;
 }
 
-// Up to `kmax` baby steps (Alg. 1 l.549-561).  Sets PH_DONE (symmetry exit) or
-// PH_GIANT (window + two more ideals stored).  Returns the steps taken.
-// List entries are gathered four at a time in registers and written with one
-// 16-byte store (per-lane lists are 16-byte aligned); a 4-byte store per step
-// makes the kernel store-transaction bound (32 lines per warp instruction).
-EIS_HD void list_flush(u32 *list, u32 n, u32 e0, u32 e1, u32 e2, u32 e3) {
-    // entries n-? .. n-1 are pending: n % 4 of them (e0 oldest); at n % 4 == 0 all four
-    const u32 k = n & 3u, b = n - (k ? k : 4u);
-    if (k == 0) {
-        *reinterpret_cast<uint4 *>(list + b) = make_uint4(e0, e1, e2, e3);
-    } else {
-        list[b] = e0;
-        if (k > 1) list[b + 1] = e1;
-        if (k > 2) list[b + 2] = e2;
-    }
+// a harmless state for lanes without a d (the lockstep loop still steps them)
+EIS_HD void win_idle(WinLane &w) {
+    w.st.sm = 0.f;
+    w.st.sp = 16777216.f;
+    w.st.Pm = 8388609.f;
+    w.st.Q = 2.f;
+    w.st.Qp = 2.f;
+    w.st.t2 = 0;
+    w.dist = 0.f;
+    w.sqd_m = -8388608.f;
+    w.Q1 = w.P1 = w.t1 = 0;
+    w.dist1 = 0.f;
+    w.res = 0;
+    w.live = false;
 }
 
-EIS_HD int bsgs_baby(BabyLane &ln, u32 *list, const BsgsArgs &B, int kmax) {
-    int k = 0;
-    // pending group: entries [n & ~3, n) live in e0..e2 (list is written up to n & ~3)
-    u32 e0 = ln.pe0, e1 = ln.pe1, e2 = ln.pe2, e3 = 0;
-    while (k < kmax) {
-        const bool ex = baby_step_fd(ln.st, ln.sqd_m, ln.dist);
-        k++;
-        const u32 e = list_entry(f_to_u(ln.st.Q), ln.st.t2 >> 1);
-        const u32 p = ln.n & 3u;
-        if (p == 0) e0 = e; else if (p == 1) e1 = e; else if (p == 2) e2 = e; else e3 = e;
-        ln.n++;
-        if (p == 3) list_flush(list, ln.n, e0, e1, e2, e3);
-        if (ex) {
-            if ((ln.n & 3u) != 0) list_flush(list, ln.n, e0, e1, e2, e3);
-            ln.res = baby_result_f(ln.st);
-            ln.phase = PH_DONE;
-            return k;
-        }
-        if (ln.extras < 0) {
-            const bool end = ln.dist >= ln.W2 || (int)ln.n >= B.cap - 2;
-            if (ln.Q1 == 0 && (end || ln.dist >= ln.W2 - ln.M2)) {
-                ln.Q1 = f_to_u(ln.st.Q);                 // mu_1 = theta_j (just stored)
-                ln.P1 = f2u_bits(ln.st.Pm) - 0x4B000000u;
-                ln.t1 = mod3(ln.st.t2 >> 1);
-                ln.dist1 = ln.dist;
-            }
-            if (end) ln.extras = 2;                      // "Compute two more ideals" (l.560)
-        } else if (--ln.extras == 0) {
-            if ((ln.n & 3u) != 0) list_flush(list, ln.n, e0, e1, e2, e3);
-            ln.phase = PH_GIANT;
-            return k;
-        }
+// One baby step (Alg. 1 l.549-556); returns the list entry of the new ideal.
+EIS_HD u32 win_step(WinLane &w) {
+    const bool ex = baby_step_fd(w.st, w.sqd_m, w.dist);
+    if (ex && w.live) {
+        w.res = baby_result_f(w.st);
+        w.live = false;
     }
-    ln.pe0 = e0;                                    // chunk end: keep the group pending
-    ln.pe1 = e1;
-    ln.pe2 = e2;
-    return k;
+    return list_entry(f_to_u(w.st.Q), w.st.t2 >> 1);
 }
 
-EIS_HD BabyRec baby_pack(const BabyLane &ln, u32 off) {
+// mu_1 = the ideal just stored (l.559)
+EIS_HD void win_mark_mu1(WinLane &w) {
+    w.Q1 = f_to_u(w.st.Q);
+    w.P1 = f2u_bits(w.st.Pm) - 0x4B000000u;
+    w.t1 = mod3(w.st.t2 >> 1);
+    w.dist1 = w.dist;
+}
+
+EIS_HD BabyRec win_pack(const WinLane &w, u32 off, u32 n) {
     BabyRec r;
     r.off = off;
-    r.n = ln.n;
-    r.Q1 = ln.Q1;
-    r.P1 = ln.P1;
-    r.t1 = ln.t1;
-    r.dist1 = ln.dist1;
-    r.dist_last = ln.dist;
+    r.n = n;
+    r.Q1 = w.Q1;
+    r.P1 = w.P1;
+    r.t1 = w.t1;
+    r.dist1 = w.dist1;
+    r.dist_last = w.dist;
     r.pad = 0;
     return r;
 }
@@ -417,7 +411,9 @@ EIS_HD int giant_hit(const GiantLane &g, int kind, u32 te, u32 t, float dist, u3
 EIS_HD GiantInfo giant_start(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmask = 0xffffffffu) {
     const GiantInfo gi = giant_advance(g, B, err, wmask);
     const float M2 = two_sided_margin2(g.d);
-    if (B.two_sided && g.dist1 >= 2.f * M2 && g.dist_last - g.dist1 >= M2) {
+    // stride shorter than the arc by >= 2M (R35), and mu''_1 = mu_1^2 beyond the
+    // window by >= M (so its direct hits are never trivial)
+    if (B.two_sided && g.dist_last - g.dist1 >= M2 && 2.f * g.dist1 - g.dist_last >= M2) {
         g.m1 = mu1_form((i64)g.Qc, (i64)g.Pc, (i64)g.d, err);
         g.t1 = g.tc;
         g.dist1 = g.distc;
@@ -430,7 +426,7 @@ EIS_HD GiantInfo giant_start(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmas
 // true when the d is decided.
 EIS_HD bool giant_lookup(GiantLane &g, const u32 *tab, const u32 *list, const BsgsArgs &B) {
     u32 te, j;
-    const int kind = store_resolve(tab, list, B.ns_log2, store_probe(tab, B.ns_log2, g.Qc), g.d,
+    const int kind = store_resolve(tab, list, B.nb, store_probe(tab, B.nb, g.Qc), g.d,
                                    (u32)g.s, g.Qc, g.Pc, te, j);
     if (kind != HIT_NONE) {
         g.phase = giant_hit(g, kind, te, g.tc, g.distc, g.Qc, g.res) ? PH_DONE : PH_HALF;
@@ -494,7 +490,7 @@ EIS_HD void giant_unpack(GiantLane &g, const GiantRec &r, u64 d) {
 }
 
 // exact half walk for one d (guard inconclusive / cap exceeded)
-EIS_HD u32 half_walk_one(u64 d, u64 &steps, u32 &err) {
+EIS_HD_COLD u32 half_walk_one(u64 d, u64 &steps, u32 &err) {
     BabyState st;
     u32 r1;
     if (baby_init(st, d, &r1)) return r1;
@@ -510,12 +506,12 @@ EIS_HD u32 half_walk_one(u64 d, u64 &steps, u32 &err) {
 // ------------------------------------------------------------------ kernels --
 struct BsgsOut {
     u32 *lists;         // [survivors][lcap] baby entries
-    u32 *tables;        // [survivors][ns] store slots
+    u32 *tables;        // [survivors][nb][BKT] store slots
     BabyRec *brecs;     // [survivors]
     GiantRec *grecs;    // [survivors]
     u32 *bqueue;        // survivor indices with a complete window
     u32 *gqueue;        // survivor indices needing giant steps
-    u32 *ctr;           // device: [0] bqueue len, [1] build work, [2] gqueue len, [3] giant work
+    u32 *ctr;           // device: [0] bqueue len, [1] unused, [2] gqueue len, [3] giant work
 };
 
 #ifdef __CUDACC__
@@ -544,153 +540,211 @@ __device__ __forceinline__ void flush_stats(const WalkArgs &a, u64 baby, u64 gia
     if (lane == 0 && s_err) atomicAdd(a.err, s_err);
 }
 
-// K3a: baby steps, per-lane refill from the survivor list.
-template <int KB>
+
+// K3a: baby steps for a wave of 32 survivors in lockstep, then their stores.
+// Shared memory per warp: the table (nb * BKT slots) and nb fill counters.
+EIS_HD u32 window_smem_words(u32 nb) { return nb * BKT + ((nb + 3) & ~3u); }
+
+__device__ __forceinline__ void store_block(u32 *dst, const u32 (&e)[8]) {
+    reinterpret_cast<uint4 *>(dst)[0] = make_uint4(e[0], e[1], e[2], e[3]);
+    reinterpret_cast<uint4 *>(dst)[1] = make_uint4(e[4], e[5], e[6], e[7]);
+}
+
+// One store, built by the whole warp in shared memory (tab: nb * BKT slots, cnt:
+// nb fill counters, both zero on entry and on exit) and written to dst.
+__device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, u32 nb, u32 *tab,
+                                            u32 *cnt, u32 *__restrict__ dst) {
+    const int lane = threadIdx.x & 31;
+    // the lists come back from DRAM (far more of them are in flight than L2
+    // holds): loads run one group of 256 entries (8 per lane) ahead
+    constexpr int G = 8;
+    u32 nx[G];
+#pragma unroll
+    for (int k = 0; k < G; k++) {
+        const u32 jn = (u32)(32 * k + lane);
+        nx[k] = jn < n ? lst[jn] : 0u;
+    }
+    for (u32 jb = 0; jb < n; jb += 32 * G) {
+        u32 cur[G];
+#pragma unroll
+        for (int k = 0; k < G; k++) {
+            cur[k] = nx[k];
+            const u32 jn = jb + 32 * (G + k) + lane;
+            nx[k] = jn < n ? lst[jn] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < G; k++) {
+            const u32 j = jb + 32 * k + lane;
+            const u32 e = cur[k];
+            const u32 sv = slot_of(e, j);
+            u32 b = store_bucket(e & 0xFFFFFu, nb);
+            bool todo = j < n;
+            // warp-uniform loop: a full bucket (rare) sends the entry onward
+            while (__any_sync(FULL_MASK, todo)) {
+                if (todo) {
+                    const u32 pos = atomicAdd(&cnt[b], 1u);
+                    if (pos < (u32)BKT) {
+                        tab[b * BKT + pos] = sv;
+                        todo = false;
+                    } else {
+                        b = next_bucket(b, nb);
+                    }
+                }
+            }
+        }
+    }
+    __syncwarp();
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    uint4 *s4 = reinterpret_cast<uint4 *>(tab);
+    for (u32 i = lane; i < nb * (BKT / 4); i += 32) {  // write out, clear for the next d
+        d4[i] = s4[i];
+        s4[i] = make_uint4(0, 0, 0, 0);
+    }
+    for (u32 i = lane; i < nb; i += 32) cnt[i] = 0;
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(256)
-bsgs_baby_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
+bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
+    extern __shared__ u32 smem[];
+    __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u32 nb = (u32)B.nb;
+    const u32 wstride = window_smem_words(nb);               // 16-byte aligned per warp
+    u32 *tab = smem + (size_t)wid * wstride;
+    u32 *cnt = tab + nb * BKT;
+    hist_zero(a, hist);
+    for (u32 i = lane; i < wstride; i += 32) tab[i] = 0;
+    __syncthreads();
+    const u32 n = *a.count;
+    const int nblk = B.nw / 8;
+    u64 baby = 0, done = 0, sym = 0;
+    for (;;) {
+        u32 wave = 0;
+        if (lane == 0) wave = atomicAdd(a.work, 1u);
+        wave = __shfl_sync(FULL_MASK, wave, 0);
+        if ((u64)wave * 32 >= n) break;
+        const u32 idx = wave * 32 + lane;
+        const bool has = idx < n;
+        u32 off = 0;
+        u64 d = 0;
+        WinLane w;
+        win_idle(w);
+        u32 e[8];
+        e[0] = e[1] = 0;
+        if (has) {
+            off = __ldg(a.list + idx);
+            d = cand_d(a.i0 + (off & ~PRIME_BIT));
+            win_begin(w, d, e[0], e[1]);
+        }
+        u32 *lst = o.lists + (u64)idx * B.lcap;
+        if (w.live) baby += 7;                           // theta_2 (closed form) + 6
+#pragma unroll
+        for (int k = 2; k < 8; k++) e[k] = win_step(w);
+        if (w.live) {
+            store_block(lst, e);
+            if (B.j1 == 7) win_mark_mu1(w);
+        }
+        for (int blk = 1; blk < nblk; blk++) {
+            if (!__any_sync(FULL_MASK, w.live)) break;
+            if (w.live) baby += 8;
+#pragma unroll
+            for (int k = 0; k < 8; k++) e[k] = win_step(w);
+            if (w.live) {
+                store_block(lst + blk * 8, e);
+                if (blk * 8 + 7 == B.j1) win_mark_mu1(w);
+            }
+        }
+        if (has && !w.live) {                            // symmetry exit (or d < 8)
+            record_result(a, hist, off, d, w.res);
+            done++;
+            sym++;
+        }
+        if (w.live) o.brecs[idx] = win_pack(w, off, (u32)B.nw);
+        const u32 live = __ballot_sync(FULL_MASK, w.live);
+        for (u32 m = live; m; m &= m - 1) {
+            const u32 i = wave * 32 + (u32)(__ffs(m) - 1);
+            build_store(o.lists + (u64)i * B.lcap, (u32)B.nw, nb, tab, cnt,
+                        o.tables + (u64)i * ((u64)nb * BKT));
+        }
+        u32 qb = 0;
+        if (lane == 0 && live) qb = atomicAdd(&o.ctr[0], (u32)__popc(live));
+        qb = __shfl_sync(FULL_MASK, qb, 0);
+        if (w.live) o.bqueue[qb + __popc(live & lanemask_lt())] = idx;
+    }
+    flush_stats(a, baby, 0, 0, done, sym, 0, 0);
+    hist_flush(a, hist);
+}
+
+// K3b: k = 2 (mu'_2 = mu_1 * mu_1: NUDUPL) for every windowed d, 32 per warp in
+// lockstep.  One-sided: the lookup of mu'_2 is left to the giant kernel's
+// pipelined probe.  Two-sided (R35): mu'_2 is the stride and mu''_1; it is
+// looked up here and mu''_2 = mu''_1^2 (NUDUPL again) taken in lockstep too.
+__global__ void __launch_bounds__(256)
+bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     __shared__ u32 hist[NROW_MAX * HIST_CAP];
     hist_zero(a, hist);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const u32 n = *a.count;
-    BabyLane ln;
-    ln.phase = PH_IDLE;
-    u32 off = 0, idx = 0;
-    u32 *list = nullptr;
-    u64 d = 0;
-    bool exhausted = false;
-    u64 baby = 0, done = 0, sym = 0;
+    const u32 nq = o.ctr[0];
+    const u32 nwarps = gridDim.x * (blockDim.x / 32);
+    u64 giant = 0, red = 0, done = 0, fb = 0, baby = 0;
     u32 err = 0;
-    for (;;) {
-        const u32 need = __ballot_sync(FULL_MASK, ln.phase == PH_IDLE && !exhausted);
-        if (need) {
-            const int leader = __ffs(need) - 1;
-            u32 base = 0;
-            if (lane == leader) base = atomicAdd(a.work, (u32)__popc(need));
-            base = __shfl_sync(FULL_MASK, base, leader);
-            if (ln.phase == PH_IDLE && !exhausted) {
-                idx = base + __popc(need & lanemask_lt());
-                if (idx < n) {
-                    off = __ldg(a.list + idx);
-                    d = cand_d(a.i0 + (off & ~PRIME_BIT));
-                    list = o.lists + (u64)idx * B.lcap;
-                    baby += 1;
-                    if (bsgs_begin(ln, list, B, d)) {
-                        record_result(a, hist, off, d, ln.res);
-                        done++;
-                        sym++;
-                        ln.phase = PH_IDLE;
-                    }
-                } else {
-                    exhausted = true;
-                }
-            }
-        }
-        if (__all_sync(FULL_MASK, exhausted && ln.phase == PH_IDLE)) break;
-        if (ln.phase == PH_BABY) {
-            baby += bsgs_baby(ln, list, B, KB);
-            if (ln.phase == PH_DONE) {
-                record_result(a, hist, off, d, ln.res);
-                done++;
-                sym++;
-                ln.phase = PH_IDLE;
-            } else if (ln.phase == PH_GIANT) {
-                o.brecs[idx] = baby_pack(ln, off);
-                o.bqueue[atomicAdd(&o.ctr[0], 1u)] = idx;
-                ln.phase = PH_IDLE;
-            }
-        }
-    }
-    flush_stats(a, baby, 0, 0, done, sym, 0, err);
-    hist_flush(a, hist);
-}
-
-// K3b: each warp builds 32 stores in shared memory, then takes k = 2 for them.
-__global__ void __launch_bounds__(256)
-bsgs_build_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
-    extern __shared__ u32 smem[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ns = 1 << B.ns_log2;
-    const u32 mask = (u32)ns - 1;
-    u32 *tab = smem + (size_t)wid * ns;
-    const u32 nb = o.ctr[0];
-    u64 giant = 0, red = 0;
-    u32 err = 0;
-    for (int i = lane; i < ns; i += 32) tab[i] = 0;
-    __syncwarp();
-    for (;;) {
-        u32 base = 0;
-        if (lane == 0) base = atomicAdd(&o.ctr[1], 32u);
-        base = __shfl_sync(FULL_MASK, base, 0);
-        if (base >= nb) break;
-        const u32 cnt = min(32u, nb - base);
-        const u32 myq = lane < (int)cnt ? o.bqueue[base + lane] : 0;
-        for (u32 q = 0; q < cnt; q++) {
-            const u32 idx = __shfl_sync(FULL_MASK, myq, q);
-            const u32 ne = o.brecs[idx].n;
-            const uint4 *l4 = reinterpret_cast<const uint4 *>(o.lists + (u64)idx * B.lcap);
-            for (u32 jb = 0; jb < ne; jb += 512) {           // up to 4 x 16 B per lane in flight
-                uint4 v[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const u32 j4 = jb / 4 + (u32)u * 32 + lane;
-                    v[u] = j4 * 4 < ne ? l4[j4] : make_uint4(0, 0, 0, 0);
-                }
-                // warp-uniform probe loops: every lane inserts its next entry and
-                // the loop runs until all lanes succeeded (a per-lane while loop
-                // leaves the warp split for the rest of the batch, measured
-                // 2.8/32 active threads)
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-#pragma unroll
-                    for (int w = 0; w < 4; w++) {
-                        const u32 j = jb + ((u32)u * 32 + lane) * 4 + w;
-                        const u32 e = w == 0 ? v[u].x : (w == 1 ? v[u].y : (w == 2 ? v[u].z : v[u].w));
-                        const u32 Q = e & 0xFFFFFu;
-                        const u32 sv = slot_entry(Q, j, mod3(e >> 20));
-                        u32 h = store_hash(Q, B.ns_log2);
-                        bool todo = j < ne;
-                        while (__any_sync(FULL_MASK, todo)) {
-                            if (todo) {
-                                if (atomicCAS(&tab[h], 0u, sv) == 0u) todo = false;
-                                else h = (h + 1) & mask;
-                            }
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            uint4 *dst = reinterpret_cast<uint4 *>(o.tables + ((u64)idx << B.ns_log2));
-            uint4 *src = reinterpret_cast<uint4 *>(tab);
-            for (int i = lane; i < ns / 4; i += 32) {        // write out, clear for the next d
-                dst[i] = src[i];
-                src[i] = make_uint4(0, 0, 0, 0);
-            }
-            __syncwarp();
-        }
-        // k = 2 (mu_2 = mu_1 * mu_1: NUDUPL) for the batch, one d per lane; the
-        // lookup of mu'_2 is left to the giant kernel's pipelined probe
-        bool push = false;
+    for (u32 base = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; base < nq;
+         base += nwarps * 32) {
+        const u32 qi = base + lane;
+        const bool has = qi < nq;
+        const u32 kmask = __ballot_sync(FULL_MASK, has);
         u32 gidx = 0;
-        const u32 kmask = __ballot_sync(FULL_MASK, lane < (int)cnt);
-        if (lane < (int)cnt) {
-            gidx = myq;
-            const BabyRec br = o.brecs[gidx];
-            GiantLane g;
+        GiantLane g;
+        g.phase = PH_IDLE;
+        BabyRec br;
+        bool two = false;
+        if (has) {
+            gidx = o.bqueue[qi];
+            br = o.brecs[gidx];
             giant_init(g, B, cand_d(a.i0 + (br.off & ~PRIME_BIT)), br, &err);
             const GiantInfo gi = giant_start(g, B, &err, kmask);
             giant++;
             red += gi.nred;
-            o.grecs[gidx] = giant_pack(g, br.off);
-            push = true;
+            two = g.m1.Q == (i64)g.Qc && g.dist1 == g.distc;   // stride = mu'_2 (R35)
         }
+        // two-sided: look up mu''_1 = mu'_2 here and take mu''_2 = mu''_1^2 (NUDUPL,
+        // the generic path) in lockstep, so the giant kernel composes distinct ideals
+        if (two) {
+            const u32 *tab = o.tables + (u64)gidx * ((u64)B.nb * BKT);
+            const u32 *lst = o.lists + (u64)gidx * B.lcap;
+            u32 te, j;
+            const int kind = store_resolve(tab, lst, B.nb, store_probe(tab, B.nb, g.Qc), g.d,
+                                           (u32)g.s, g.Qc, g.Pc, te, j);
+            if (kind != HIT_NONE)
+                g.phase = giant_hit(g, kind, te, g.tc, g.distc, g.Qc, g.res) ? PH_DONE : PH_HALF;
+        }
+        const u32 amask = __ballot_sync(FULL_MASK, two && g.phase == PH_GIANT);
+        if (two && g.phase == PH_GIANT) {
+            const GiantInfo gi = giant_advance(g, B, &err, amask);
+            giant++;
+            red += gi.nred;
+        }
+        if (g.phase == PH_HALF) {                              // inconclusive guard (tiny d)
+            fb++;
+            g.res = half_walk_one(g.d, baby, err);
+            g.phase = PH_DONE;
+        }
+        if (g.phase == PH_DONE) {
+            record_result(a, hist, br.off, g.d, g.res);
+            done++;
+        }
+        const bool push = has && g.phase == PH_GIANT;
+        if (push) o.grecs[gidx] = giant_pack(g, br.off);
         const u32 pm = __ballot_sync(FULL_MASK, push);
         u32 qb = 0;
         if (lane == 0 && pm) qb = atomicAdd(&o.ctr[2], (u32)__popc(pm));
         qb = __shfl_sync(FULL_MASK, qb, 0);
         if (push) o.gqueue[qb + __popc(pm & lanemask_lt())] = gidx;
     }
-    flush_stats(a, 0, giant, red, 0, 0, 0, err);
+    flush_stats(a, baby, giant, red, done, 0, fb, err);
+    hist_flush(a, hist);
 }
 
 // K3c: giant steps with per-lane refill and a pipelined lookup.
@@ -724,7 +778,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                     const GiantRec r = o.grecs[idx];
                     off = r.off;                          // (with the prime bit)
                     giant_unpack(g, r, cand_d(a.i0 + (off & ~PRIME_BIT)));
-                    tab = o.tables + ((u64)idx << B.ns_log2);
+                    tab = o.tables + (u64)idx * ((u64)B.nb * BKT);
                     list = o.lists + (u64)idx * B.lcap;
                 } else {
                     exhausted = true;
@@ -738,12 +792,12 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             // probed) while computing mu'_{k+1}
             const u32 pQ = g.Qc, pP = g.Pc, pt = g.tc;
             const float pdist = g.distc;
-            const Probe pr = store_probe(tab, B.ns_log2, pQ);
+            const Probe pr = store_probe(tab, B.nb, pQ);
             const GiantInfo gi = giant_advance(g, B, &err, gmask);
             giant++;
             red += gi.nred;
             u32 te, j;
-            const int kind = store_resolve(tab, list, B.ns_log2, pr, g.d, (u32)g.s, pQ, pP, te, j);
+            const int kind = store_resolve(tab, list, B.nb, pr, g.d, (u32)g.s, pQ, pP, te, j);
             warp_reconverge(gmask);
             if (kind != HIT_NONE) {
                 g.phase = giant_hit(g, kind, te, pt, pdist, pQ, g.res) ? PH_DONE : PH_HALF;
@@ -792,22 +846,38 @@ inline void bsgs_free(BsgsScratch &s) {
     s = BsgsScratch();
 }
 
-constexpr int BSGS_KB = 32;
 constexpr int BSGS_THREADS = 256;
 
-// Store sizes for a segment whose largest d is d_max: ~1.22 nats per baby step
-// (SURVEY.md A.8), cap ~ the window's entry count + slack (R33: a lower cap
-// only ends the window early), table load <= ~0.55.
+// Window and store sizes for a segment whose largest d is d_max.  nw ~ the
+// alpha d^(1/4)-nat window at ~1.22 nats per baby step, a
+// multiple of 8.  mu_1 (j1, the end of a block): two-sided (R35), the last block
+// end ~1.25 M nats of steps before the window end; one-sided (the paper's Alg. 1,
+// or windows too short for both margins), the last block end that leaves >= 2
+// more ideals (l.560).
 struct BsgsSizes {
-    int ns_log2, cap, lcap;
+    int nw, j1, nb, lcap;
 };
-inline BsgsSizes bsgs_sizes(u64 d_max, float alpha) {
+inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
     BsgsSizes z;
     const double w = alpha * std::pow((double)d_max, 0.25);   // window in nats
-    z.cap = std::min(2040, (int)(w / 1.22 * 1.05) + 8);
-    z.ns_log2 = 6;
-    while ((double)(1 << z.ns_log2) < 1.8 * z.cap && z.ns_log2 < 12) z.ns_log2++;
-    z.lcap = (z.cap + 31) & ~31;
+    z.nw = std::min(2040, std::max(16, ((int)(w / 1.22) + 7) & ~7));
+    const double lnd = std::log((double)d_max);
+    const double M = 2.0 * lnd + 4.0;
+    const double msteps = 1.25 * M / 1.22;                      // M nats with slack
+    // one-sided: mu_1 at a block end, then 8 more ideals (>= the 2 of l.560);
+    // mu'_2 = mu_1^2 lands beyond the window when dist_1 > 8 steps + kappa
+    // (kappa < ln d), so tiny windows are widened to that (R6: results unchanged)
+    const int j1min = (((int)std::ceil((lnd + 4.0) / 1.22 + 8.0) + 1 + 7) & ~7) - 1;
+    z.j1 = std::max(z.nw - 9, j1min);
+    z.nw = std::min(2040, z.j1 + 9);
+    if (two_sided) {
+        // mu_1 = theta_{j1+1} needs dist_last - dist_1 >= M and 2 dist_1 - dist_last
+        // >= M (giant_start checks both per d; they fail only in the tails)
+        const int j = ((z.nw - (int)std::ceil(msteps)) & ~7) - 1;
+        if (j >= 7 && z.nw - j >= msteps && 2 * j - z.nw >= msteps) z.j1 = j;
+    }
+    z.nb = std::max(1, (int)std::ceil(z.nw / (BKT * BKT_LOAD)));
+    z.lcap = (z.nw + 31) & ~31;
     return z;
 }
 
@@ -825,32 +895,32 @@ inline int bsgs_grow(T *&p, size_t &cap, size_t n) {
 struct BsgsPlan {
     BsgsArgs B;
     BsgsOut o;
-    size_t build_smem;
-    unsigned baby_blocks, build_blocks, giant_blocks;
+    size_t window_smem;
+    unsigned window_blocks, prep_blocks, giant_blocks;
 };
 
-inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha) {
-    const BsgsSizes z = bsgs_sizes(d_max, alpha);
-    return (size_t)4 * z.lcap + ((size_t)4 << z.ns_log2) + sizeof(BabyRec) + sizeof(GiantRec) + 8;
+inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
+    const BsgsSizes z = bsgs_sizes(d_max, alpha, two_sided);
+    return (size_t)4 * z.lcap + (size_t)64 * z.nb + sizeof(BabyRec) + sizeof(GiantRec) + 8;
 }
 
 #ifdef __CUDACC__
 // Size one segment buffer (seg_len candidates bound the survivors) and choose
-// the launch shapes.  ctr: 4 device counters (zeroed by bsgs_launch_baby).
+// the launch shapes.  ctr: 4 device counters (zeroed by bsgs_launch_window).
 inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
                         int giant_ctas, int two_sided, BsgsScratch &scr, u32 *ctr) {
     BsgsArgs &B = pl.B;
-    B.two_sided = two_sided;
-    B.alpha = alpha_x16 / 16.0f;
-    const BsgsSizes z = bsgs_sizes(d_hi, B.alpha);
-    B.ns_log2 = z.ns_log2;
-    B.cap = z.cap;
+    const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided);
+    B.nw = z.nw;
+    B.j1 = z.j1;
+    B.nb = z.nb;
     B.lcap = z.lcap;
     B.plain_th = 50;
     B.giant_cap_mul = 20.0f;
+    B.two_sided = two_sided;
     const size_t n = (size_t)seg_len;
     if (bsgs_grow(scr.lists, scr.lists_n, n * (size_t)z.lcap)) return -3;
-    if (bsgs_grow(scr.tables, scr.tables_n, n << z.ns_log2)) return -3;
+    if (bsgs_grow(scr.tables, scr.tables_n, n * (size_t)z.nb * BKT)) return -3;
     if (bsgs_grow(scr.brecs, scr.brecs_n, n)) return -3;
     if (bsgs_grow(scr.grecs, scr.grecs_n, n)) return -3;
     if (bsgs_grow(scr.bqueue, scr.bqueue_n, n)) return -3;
@@ -864,20 +934,20 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     o.gqueue = scr.gqueue;
     o.ctr = ctr;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_baby_kernel<BSGS_KB>,
-                                                      BSGS_THREADS, 0) != cudaSuccess ||
+    pl.window_smem = (size_t)(BSGS_THREADS / 32) * window_smem_words((u32)z.nb) * sizeof(u32);
+    if (cudaFuncSetAttribute(bsgs_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pl.window_smem) != cudaSuccess)
+        return -4;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_window_kernel, BSGS_THREADS,
+                                                      pl.window_smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
-    pl.baby_blocks = (unsigned)(num_sms * per_sm);
-    pl.build_smem = (size_t)(BSGS_THREADS / 32) * ((size_t)4 << z.ns_log2);
-    if (cudaFuncSetAttribute(bsgs_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pl.build_smem) != cudaSuccess)
-        return -4;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_build_kernel, BSGS_THREADS,
-                                                      pl.build_smem) != cudaSuccess ||
+    pl.window_blocks = (unsigned)(num_sms * per_sm);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_prep_kernel, BSGS_THREADS,
+                                                      0) != cudaSuccess ||
         per_sm < 1)
         return -4;
-    pl.build_blocks = (unsigned)(num_sms * per_sm);
+    pl.prep_blocks = (unsigned)(num_sms * per_sm);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_giant_kernel, BSGS_THREADS,
                                                       0) != cudaSuccess ||
         per_sm < 1)
@@ -886,12 +956,12 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     return 0;
 }
 
-// baby + build on the main stream
+// window + prep on the main stream
 inline int bsgs_launch_baby(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t s) {
     if (cudaMemsetAsync(pl.o.ctr, 0, 4 * sizeof(u32), s) != cudaSuccess) return -4;
-    bsgs_baby_kernel<BSGS_KB><<<pl.baby_blocks, BSGS_THREADS, 0, s>>>(a, pl.B, pl.o);
+    bsgs_window_kernel<<<pl.window_blocks, BSGS_THREADS, pl.window_smem, s>>>(a, pl.B, pl.o);
     if (cudaGetLastError() != cudaSuccess) return -4;
-    bsgs_build_kernel<<<pl.build_blocks, BSGS_THREADS, pl.build_smem, s>>>(a, pl.B, pl.o);
+    bsgs_prep_kernel<<<pl.prep_blocks, BSGS_THREADS, 0, s>>>(a, pl.B, pl.o);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 

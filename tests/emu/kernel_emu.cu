@@ -3,7 +3,8 @@
 // CPU, one d at a time, so their arithmetic can be checked against the oracle
 // without a GPU.  Not part of the product library.
 //
-// usage: kernel_emu MODE ALPHA_X16 NS_LOG2 [PLAIN_TH [TWO_SIDED]] < d-list  (MODE: half | bsgs)
+// usage: kernel_emu MODE ALPHA_X16 NB [PLAIN_TH [TWO_SIDED]] < d-list  (MODE: half | bsgs;
+//        NB: table buckets per d, 0 = sized from d; half mode: 99 = integer step)
 // prints per d: "d t baby giant reduce fallback err kinds(plain,comp,dupl)"
 #include <cstdio>
 #include <cstdlib>
@@ -20,13 +21,13 @@ int main(int argc, char **argv) {
     }
     const bool bsgs = strcmp(argv[1], "bsgs") == 0;
     BsgsArgs B;
-    B.alpha = atoi(argv[2]) / 16.0f;
-    const int ns_fixed = atoi(argv[3]);
+    const float alpha = atoi(argv[2]) / 16.0f;
+    const int nb_fixed = atoi(argv[3]);
     B.plain_th = argc > 4 ? atoi(argv[4]) : 50;
     B.giant_cap_mul = 20.0f;
     B.two_sided = argc > 5 ? atoi(argv[5]) : 1;
     std::vector<u32> bm(1 << 10);
-    std::vector<u32> tab(1 << 14), lst(1 << 12);
+    std::vector<u32> tab(1 << 16), lst(1 << 12);
     unsigned long long d;
     while (scanf("%llu", &d) == 1) {
         u32 res = 0, err = 0;
@@ -36,7 +37,7 @@ int main(int argc, char **argv) {
             u32 r1;
             baby = 1;
             if (baby_init(st, d, &r1)) res = r1;
-            else if (ns_fixed == 99) {                      // integer form of the step
+            else if (nb_fixed == 99) {                      // integer form of the step
                 for (;;) { baby++; if (baby_step(st)) break; }
                 res = baby_result(st);
             } else {                                        // FP32 form (the kernel's)
@@ -45,25 +46,33 @@ int main(int argc, char **argv) {
                 res = baby_result_f(sf);
             }
         } else {
-            const BsgsSizes z = bsgs_sizes(d, B.alpha);
-            B.ns_log2 = ns_fixed ? ns_fixed : z.ns_log2;
-            B.cap = ns_fixed ? (1 << ns_fixed) / 2 - 2 : z.cap;
-            B.lcap = (B.cap + 31) & ~31;
-            std::fill(tab.begin(), tab.begin() + (1 << B.ns_log2), 0u);
-            BabyLane ln;
+            const BsgsSizes z = bsgs_sizes(d, alpha, B.two_sided);
+            B.nw = z.nw;
+            B.j1 = z.j1;
+            B.nb = nb_fixed ? nb_fixed : z.nb;
+            B.lcap = z.lcap;
+            std::fill(tab.begin(), tab.begin() + (size_t)B.nb * BKT, 0u);
+            WinLane w;
+            u32 e0, e1;
             baby = 1;
-            if (bsgs_begin(ln, lst.data(), B, d)) {
-                res = ln.res;
-            } else {
-                while (ln.phase == PH_BABY) baby += bsgs_baby(ln, lst.data(), B, 8);
-                if (ln.phase == PH_DONE) {
-                    res = ln.res;
+            if (!win_begin(w, d, e0, e1)) {
+                res = w.res;
+            } else {                                        // window kernel, one lane
+                lst[0] = e0;
+                lst[1] = e1;
+                for (int j = 2; j < B.nw && w.live; j++) {
+                    lst[j] = win_step(w);
+                    baby++;
+                    if (j == B.j1 && w.live) win_mark_mu1(w);
+                }
+                if (!w.live) {
+                    res = w.res;
                 } else {
-                    store_build_seq(tab.data(), B.ns_log2, lst.data(), ln.n);
-                    const BabyRec br = baby_pack(ln, 0);
+                    store_build_seq(tab.data(), (u32)B.nb, lst.data(), (u32)B.nw);
+                    const BabyRec br = win_pack(w, 0, (u32)B.nw);
                     GiantLane g;
                     giant_init(g, B, d, br, &err);
-                    GiantInfo gi = giant_start(g, B, &err);   // k = 2 (build kernel)
+                    GiantInfo gi = giant_start(g, B, &err);   // prep kernel
                     giant++;
                     red += gi.nred;
                     kinds[gi.kind]++;
