@@ -41,7 +41,8 @@ SM_MAX_MHZ_FALLBACK = 1965.0
 # generic u32 step is 34 instructions; `work_equiv_generic` reports that view.
 OPS_PER_BABY = 14
 GENERIC_PER_BABY = 34
-OPS_PER_GIANT = 700    # measured thread-instructions per giant step (K3 BSGS)
+OPS_PER_GIANT = 700    # thread-instructions of one fast-path giant step (K3 BSGS)
+OPS_PER_ENTRY = 12     # store insert per window entry: slot pack, hash, bucket insert
 
 
 def _env_int(k, d):
@@ -230,6 +231,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     walk_ms, launches, stats = [], 0, {}
+    kern_ms = {"sieve": [], "window": [], "giant": []}
     cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
     sampler = ClockSampler(int(cvd.split(",")[gpu]) if cvd else gpu)
     sampler.start()
@@ -243,6 +245,8 @@ def main():
         ev[k][1].record(stream)
         stats = eis.get_stats()
         walk_ms.append(stats["walk_ms"])
+        for kn in kern_ms:
+            kern_ms[kn].append(stats[f"{kn}_ms"])
         launches += int(stats["kernel_launches"]) + 1      # + prefix kernel
         flush.fill_(k)                                      # untimed: evict L2
     torch.cuda.synchronize()
@@ -253,10 +257,12 @@ def main():
     tot_ms = sum(step_ms)
     res = buckets.cpu().numpy().astype(np.uint64)
 
-    t = torch.tensor([tot_ms, float(np.mean(walk_ms))], dtype=torch.float64, device=dev)
+    t = torch.tensor([tot_ms, float(np.mean(walk_ms))] + [float(np.mean(v)) for v in kern_ms.values()],
+                     dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms_max, walk_ms_max = float(t[0]), float(t[1])
+    kms = dict(zip(kern_ms, (float(v) for v in t[2:])))
 
     # verification of the bench output itself: Table 1 window (9.9e9, 1e10]
     i99 = list(x).index(9_900_000_000)
@@ -284,16 +290,38 @@ def main():
 
     if rank == 0:
         value = nD_job / (tot_ms_max / args.steps / 1e3)
-        ops_per_launch = OPS_PER_BABY * stats["baby_steps"] + OPS_PER_GIANT * stats["giant_steps"]
-        achieved = ops_per_launch / (walk_ms_max / 1e3) / 1e12     # Tops/s (thread-ops)
-        sm_clk = SM_MAX_MHZ_FALLBACK
+        sm_clk = clocks.get("sm_mhz") or SM_MAX_MHZ_FALLBACK
         peak = 148 * 4 * 32 * sm_clk * 1e6 / 1e12                 # issue-slot peak, Tops/s
+        bsgs = stats["giant_steps"] > 0
+        # algorithmic thread-ops of each kernel family in one step (this rank)
+        entries = stats["baby_steps"] if bsgs else 0              # one store entry per step
+        kops = {"window": OPS_PER_BABY * stats["baby_steps"] + OPS_PER_ENTRY * entries,
+                "giant": OPS_PER_GIANT * stats["giant_steps"]}
+        per_kernel = {k: {"ms": kms[k], "tops": kops[k] / (kms[k] / 1e3) / 1e12 if kms[k] else None}
+                      for k in kops}
+        for k in per_kernel:
+            if per_kernel[k]["tops"] is not None:
+                per_kernel[k]["frac"] = per_kernel[k]["tops"] / peak
+        per_kernel["sieve"] = {"ms": kms["sieve"]}
+        if bsgs:
+            # the BSGS kernels run on two streams and overlap (the giant kernel of one
+            # segment with the window kernel of the next), so the walk is the unit:
+            # all of its algorithmic ops over its device time
+            ops_per_launch = kops["window"] + kops["giant"]
+            achieved = ops_per_launch / (walk_ms_max / 1e3) / 1e12
+            dom_name = "BSGS walk: bsgs_window_kernel + bsgs_prep_kernel + bsgs_giant_kernel"
+            dom_ms = walk_ms_max
+        else:
+            ops_per_launch = kops["window"]
+            achieved = per_kernel["window"]["tops"]
+            dom_name = "walk_half_kernel"
+            dom_ms = kms["window"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "u32" if stats["giant_steps"] == 0 else "u32+i64",
+            "dtype": "f32" if stats["giant_steps"] == 0 else "f32+f64",   # exact-integer FP
             "data": "synthetic",
             "config": {
                 "workload": f"all d = 5 mod 8 in ({jlo}, {jhi}] ({nD_job} d in D); rank r owns "
@@ -310,20 +338,26 @@ def main():
                     else f"count_window_distributed (C ABI dev + {args.backend} allreduce)"},
             "gpu_launches": launches,
             "roofline": {
-                "bound": "alu", "kernel": "walk (K3+K4)",
+                "bound": "alu", "kernel": dom_name,
                 "achieved": achieved, "peak": peak, "unit": "Tops/s", "frac": achieved / peak,
-                "traffic": 50.8e6 if stats["giant_steps"] == 0 else None,
-                "traffic_note": "dram read+write bytes per walk launch, ncu --set full "
+                "traffic": None if bsgs else 50.8e6,
+                "traffic_note": ("see profiles/ (ncu --set full of the BSGS kernels); the path "
+                                 "is issue-bound, DRAM < 40% of peak") if bsgs else
+                                "dram read+write bytes per walk launch, ncu --set full "
                                 "(profiles/r01_half_walk.txt); algorithmic bytes = 4 per d "
                                 "(survivor list) = 50.7 MB",
-                "work_equiv_generic": (GENERIC_PER_BABY * stats["baby_steps"] + OPS_PER_GIANT
-                                       * stats["giant_steps"]) / (walk_ms_max / 1e3) / 1e12 / peak,
-                "ops_per_launch": ops_per_launch,
-                "walk_ms_per_launch": walk_ms_max,
+                "ops_per_step": ops_per_launch,
+                "kernel_ms_per_step": dom_ms,
+                "per_kernel": per_kernel,
+                "work_equiv_generic": None if bsgs else
+                (GENERIC_PER_BABY * stats["baby_steps"]) / (kms["window"] / 1e3) / 1e12 / peak,
+                "walk_ms_per_step": walk_ms_max,
                 "walk_share_of_step": walk_ms_max / (tot_ms_max / args.steps),
-                "basis": f"{OPS_PER_BABY} SASS instructions per rho step, {OPS_PER_GIANT} "
-                         f"thread-instructions per giant step; peak = 148 SM x 4 SMSP x 32 "
-                         f"lanes x {sm_clk:.0f} MHz issue slots (DESIGN.md 4)",
+                "basis": f"thread-ops per unit: {OPS_PER_BABY} per rho step, {OPS_PER_ENTRY} per "
+                         f"store entry, {OPS_PER_GIANT} per giant step; kernel time = summed CUDA "
+                         f"events around its launches on its own stream (BSGS: the walk's span, "
+                         f"per_kernel spans overlap); peak = 148 SM x 4 SMSP x "
+                         f"32 lanes x {sm_clk:.0f} MHz (sampled SM clock) issue slots (DESIGN.md 4)",
             },
             "clocks": clocks,
             "stats_per_rank_step": {k: stats[k] for k in ("d_classified", "baby_steps",

@@ -174,6 +174,9 @@ typedef struct {
     uint64_t kernel_launches;/* kernels launched by the last call */
     double walk_ms;          /* device time of the segment loop: sieve + walk kernels (CUDA events) */
     double total_ms;         /* device time of the whole call */
+    double sieve_ms;         /* summed device time of the sieve kernels (events on their stream) */
+    double window_ms;        /* ... of the HALF walk kernels, or of the BSGS window + prep kernels */
+    double giant_ms;         /* ... of the BSGS giant kernels (aux stream; overlaps the others) */
 } eis_stats;
 
 /* Counters of the most recent compute call (synchronises the device). */

@@ -24,7 +24,8 @@ __all__ = [
     "MAX_D", "LIB_PATH",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libeis.so")
+LIB_PATH = os.environ.get("EIS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "libeis.so")   # EIS_LIB: build experiments
 MAX_D = 100_000_000_000
 NOT_IN_D = 0xFF
 MODE_AUTO, MODE_HALF, MODE_BSGS = 0, 1, 2
@@ -59,6 +60,9 @@ class Stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_uint64),
         ("walk_ms", ctypes.c_double),
         ("total_ms", ctypes.c_double),
+        ("sieve_ms", ctypes.c_double),
+        ("window_ms", ctypes.c_double),
+        ("giant_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -55,9 +55,11 @@ struct Ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // options
     int mode = EIS_MODE_AUTO;
-    u64 crossover = ~0ULL;           // AUTO: HALF below, BSGS at/above (measured: HALF is faster
-                                     // at every d <= 1e11 on B200)
-    int alpha_x16 = 16;              // BSGS baby window W = alpha * d^(1/4)
+    u64 crossover = 8000000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
+                                     // HALF 2.0x faster at 1e9, BSGS 1.02x at 1e10, 1.35x
+                                     // at 3e10, 1.76x at 1e11)
+    int alpha_x16 = 28;              // BSGS baby window W = alpha * d^(1/4) (best at 1e10,
+                                     // within 1% of the best at 1e11)
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
     int threads = 256;
@@ -68,10 +70,27 @@ struct Ctx {
     eis_stats last{};
     float walk_ms_acc = 0.f;
     int launches = 0;
+    // per-kernel device time: event pairs around each launch, summed at the end
+    // of run_range (the events are complete then)
+    std::vector<cudaEvent_t> kev;
+    std::vector<std::pair<int, int>> kspan[3];     // [0] sieve, [1] window+prep / half, [2] giant
+    int kev_used = 0;
+    double kms[3] = {0, 0, 0};
 };
 
 Ctx g;
 thread_local std::string g_err;
+
+// next event of the per-kernel timing pool (created on first use)
+cudaEvent_t kev_next(int &idx) {
+    if (g.kev_used == (int)g.kev.size()) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        g.kev.push_back(e);
+    }
+    idx = g.kev_used++;
+    return g.kev[idx];
+}
 
 int fail(int code, const char *fmt, ...) {
     char buf[512];
@@ -244,11 +263,15 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         CUDA_TRY(cudaMemsetAsync(bf.ctr, 0, 8 * sizeof(u32), s));
         const unsigned sblocks = (unsigned)((len + SIEVE_CHUNK - 1) / SIEVE_CHUNK);
         u8 *fseg = flags_dev ? flags_dev + (seg - i_first) : nullptr;
+        int e0, e1;
+        CUDA_TRY(cudaEventRecord(kev_next(e0), s));
         sieve_compact_kernel<<<sblocks, SIEVE_THREADS,
                                (with_primes ? 2 : 1) * SIEVE_WORDS * sizeof(u32), s>>>(
             seg, len, g.d_primes, std::min(n_small, n_primes), n_primes, bf.list, bf.ctr, fseg,
             with_primes, std::min(n_small1, n_primes));
         CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(kev_next(e1), s));
+        g.kspan[0].push_back({e0, e1});
         g.launches++;
 
         WalkArgs a;
@@ -267,22 +290,33 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.stats = g.d_stats;
         if (bsgs) {
             BsgsPlan pl;
-            CUDA_TRY(cudaStreamSynchronize(g.aux));     // scratch may be (re)allocated below
+            // scratch is (re)allocated only when it must grow: drain both streams then
+            // (otherwise the giant kernel of the previous segment keeps running on aux)
+            if (bsgs_needs_grow(bf.bsgs, len, d_last, g.alpha_x16, g.two_sided)) {
+                CUDA_TRY(cudaStreamSynchronize(g.aux));
+                CUDA_TRY(cudaStreamSynchronize(s));
+            }
             int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.giant_ctas, g.two_sided, bf.bsgs,
                                   bf.ctr + 2);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
+            CUDA_TRY(cudaEventRecord(kev_next(e0), s));
             if (bsgs_launch_baby(a, pl, s))
                 return fail(EIS_EDEVICE, "BSGS baby launch failed: %s",
                             cudaGetErrorString(cudaGetLastError()));
-            g.launches++;
+            g.launches += 2;                            // window + prep
+            CUDA_TRY(cudaEventRecord(kev_next(e1), s));
+            g.kspan[1].push_back({e0, e1});
             CUDA_TRY(cudaEventRecord(bf.baby_done, s));
             CUDA_TRY(cudaStreamWaitEvent(g.aux, bf.baby_done, 0));
+            CUDA_TRY(cudaEventRecord(kev_next(e0), g.aux));
             if (bsgs_launch_giant(a, pl, g.aux))
                 return fail(EIS_EDEVICE, "BSGS giant launch failed: %s",
                             cudaGetErrorString(cudaGetLastError()));
             g.launches++;
+            CUDA_TRY(cudaEventRecord(kev_next(e1), g.aux));
+            g.kspan[2].push_back({e0, e1});
             CUDA_TRY(cudaEventRecord(bf.giant_done, g.aux));
             used_aux = true;
         } else {
@@ -294,6 +328,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
                 const double exp_steps = 0.07 * std::sqrt((double)cand_d(seg));
                 ks = exp_steps >= 8 * 144 ? 144 : exp_steps >= 8 * 72 ? 72 : exp_steps >= 8 * 36 ? 36 : 18;
             }
+            CUDA_TRY(cudaEventRecord(kev_next(e0), s));
             switch (ks) {
                 case 18: walk_half_kernel<18><<<wblocks, 256, 0, s>>>(a); break;
                 case 72: walk_half_kernel<72><<<wblocks, 256, 0, s>>>(a); break;
@@ -301,6 +336,8 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
                 default: walk_half_kernel<36><<<wblocks, 256, 0, s>>>(a); break;
             }
             CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaEventRecord(kev_next(e1), s));
+            g.kspan[1].push_back({e0, e1});
             g.launches++;
         }
         seg += len;
@@ -314,6 +351,15 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     float ms = 0;
     cudaEventElapsedTime(&ms, g.ev[2], g.ev[3]);
     g.walk_ms_acc += ms;
+    for (int k = 0; k < 3; k++) {
+        for (auto &pr : g.kspan[k]) {
+            float t = 0;
+            if (cudaEventElapsedTime(&t, g.kev[pr.first], g.kev[pr.second]) == cudaSuccess)
+                g.kms[k] += t;
+        }
+        g.kspan[k].clear();
+    }
+    g.kev_used = 0;
     u32 err = 0;
     CUDA_TRY(cudaMemcpy(&err, g.d_err, sizeof(u32), cudaMemcpyDeviceToHost));
     if (err) return fail(EIS_EINTERNAL, "%u in-kernel invariant violations in [%llu, %llu]", err,
@@ -349,6 +395,7 @@ __global__ void prefix_kernel(const u64 *in, u64 *out, int n, int nrow) {
 int begin_call(cudaStream_t s) {
     g.walk_ms_acc = 0;
     g.launches = 0;
+    g.kms[0] = g.kms[1] = g.kms[2] = 0;
     CUDA_TRY(cudaMemsetAsync(g.d_stats, 0, ST_NSLOTS * sizeof(u64), s));
     CUDA_TRY(cudaMemsetAsync(g.d_err, 0, sizeof(u32), s));
     CUDA_TRY(cudaEventRecord(g.ev[0], s));
@@ -371,6 +418,9 @@ int end_call(cudaStream_t s) {
     g.last.kernel_launches = (u64)g.launches;
     g.last.walk_ms = g.walk_ms_acc;
     g.last.total_ms = ms;
+    g.last.sieve_ms = g.kms[0];
+    g.last.window_ms = g.kms[1];
+    g.last.giant_ms = g.kms[2];
     return 0;
 }
 
@@ -439,6 +489,7 @@ void eis_finalize(void) {
     cudaFree(g.d_buckets);
     cudaFree(g.d_stats);
     for (auto &ev : g.ev) if (ev) cudaEventDestroy(ev);
+    for (auto &ev : g.kev) cudaEventDestroy(ev);
     if (g.stream) cudaStreamDestroy(g.stream);
     if (g.aux) cudaStreamDestroy(g.aux);
     Ctx fresh;

@@ -193,9 +193,10 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
 }
 
 // ----------------------------------------------------------- window phase --
-// Baby steps in the half walk's exact FP32 form (walk_half.cuh) plus the log2
-// distance of each generator multiplier (P_j + sqrt d)/Q_{j-1}.
-EIS_HD bool baby_step_fd(BabyStateF &st, float sqd_m, float &dist) {
+// Baby steps in the half walk's exact FP32 form (walk_half.cuh) plus the
+// generator multiplier (P_j + sqrt d)/Q_{j-1}, multiplied into `prod`; its log2
+// is added to the distance every 4 steps (win_flush: 4 multipliers < d^2 < 2^74).
+EIS_HD bool baby_step_fd(BabyStateF &st, float sqd_m, float &prod) {
     const float num = st.Pm + st.sm;
     const float rq = rcp_approx(st.Q);
     const float rqb = rq * 1.000000476837158203125f;
@@ -204,7 +205,7 @@ EIS_HD bool baby_step_fd(BabyStateF &st, float sqd_m, float &dist) {
     const float Pnm = st.sp - r;
     const float Qn = fmaf(q, st.Pm - Pnm, st.Qp);
     st.t2 += (f2u_bits(Pnm) & 2u) + 2u;
-    dist += log2_approx((Pnm + sqd_m) * rq);
+    prod *= (Pnm + sqd_m) * rq;
     const bool eP = (Pnm == st.Pm);
     st.Qp = st.Q;
     st.Q = Qn;
@@ -217,7 +218,8 @@ EIS_HD u32 f_to_u(float v) { return f2u_bits(v + 8388608.0f) - 0x4B000000u; }   
 
 struct WinLane {
     BabyStateF st;
-    float dist;         // log2 theta_{j+1} of the current ideal
+    float dist;         // log2 theta_{j+1} of the current ideal (after win_flush)
+    float prod;         // multipliers not yet in dist
     float sqd_m;        // sqrt(d) - 2^23 (P + sqrt d = Pm + sqd_m)
     u32 Q1, P1, t1;     // mu_1
     float dist1;
@@ -249,6 +251,7 @@ EIS_HD bool win_begin(WinLane &w, u64 d, u32 &e0, u32 &e1) {
     e0 = list_entry(2u, 0u);
     e1 = list_entry(b.Q, b.t2 >> 1);
     w.dist = log2_approx(((float)b.P + sqd) * 0.5f);
+    w.prod = 1.f;
     w.Q1 = 0;
     w.live = true;
     return true;
@@ -263,6 +266,7 @@ EIS_HD void win_idle(WinLane &w) {
     w.st.Qp = 2.f;
     w.st.t2 = 0;
     w.dist = 0.f;
+    w.prod = 1.f;
     w.sqd_m = -8388608.f;
     w.Q1 = w.P1 = w.t1 = 0;
     w.dist1 = 0.f;
@@ -272,7 +276,7 @@ EIS_HD void win_idle(WinLane &w) {
 
 // One baby step (Alg. 1 l.549-556); returns the list entry of the new ideal.
 EIS_HD u32 win_step(WinLane &w) {
-    const bool ex = baby_step_fd(w.st, w.sqd_m, w.dist);
+    const bool ex = baby_step_fd(w.st, w.sqd_m, w.prod);
     if (ex && w.live) {
         w.res = baby_result_f(w.st);
         w.live = false;
@@ -280,7 +284,13 @@ EIS_HD u32 win_step(WinLane &w) {
     return list_entry(f_to_u(w.st.Q), w.st.t2 >> 1);
 }
 
-// mu_1 = the ideal just stored (l.559)
+// fold the pending multipliers into the distance (every 4 steps: entry j = 3 mod 4)
+EIS_HD void win_flush(WinLane &w) {
+    w.dist += log2_approx(w.prod);
+    w.prod = 1.f;
+}
+
+// mu_1 = the ideal just stored (l.559); after win_flush
 EIS_HD void win_mark_mu1(WinLane &w) {
     w.Q1 = f_to_u(w.st.Q);
     w.P1 = f2u_bits(w.st.Pm) - 0x4B000000u;
@@ -578,16 +588,21 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
             const u32 e = cur[k];
             const u32 sv = slot_of(e, j);
             u32 b = store_bucket(e & 0xFFFFFu, nb);
-            bool todo = j < n;
-            // warp-uniform loop: a full bucket (rare) sends the entry onward
-            while (__any_sync(FULL_MASK, todo)) {
-                if (todo) {
+            // one attempt; a full bucket (rare at load 0.62) sends the entry onward
+            // in a warp-uniform slow loop
+            bool ovf = false;
+            if (j < n) {
+                const u32 pos = atomicAdd(&cnt[b], 1u);
+                if (pos < (u32)BKT) tab[b * BKT + pos] = sv;
+                else ovf = true;
+            }
+            while (__any_sync(FULL_MASK, ovf)) {
+                if (ovf) {
+                    b = next_bucket(b, nb);
                     const u32 pos = atomicAdd(&cnt[b], 1u);
                     if (pos < (u32)BKT) {
                         tab[b * BKT + pos] = sv;
-                        todo = false;
-                    } else {
-                        b = next_bucket(b, nb);
+                        ovf = false;
                     }
                 }
             }
@@ -640,7 +655,10 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         u32 *lst = o.lists + (u64)idx * B.lcap;
         if (w.live) baby += 7;                           // theta_2 (closed form) + 6
 #pragma unroll
-        for (int k = 2; k < 8; k++) e[k] = win_step(w);
+        for (int k = 2; k < 8; k++) {
+            e[k] = win_step(w);
+            if (k == 3 || k == 7) win_flush(w);
+        }
         if (w.live) {
             store_block(lst, e);
             if (B.j1 == 7) win_mark_mu1(w);
@@ -649,7 +667,10 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             if (!__any_sync(FULL_MASK, w.live)) break;
             if (w.live) baby += 8;
 #pragma unroll
-            for (int k = 0; k < 8; k++) e[k] = win_step(w);
+            for (int k = 0; k < 8; k++) {
+                e[k] = win_step(w);
+                if (k == 3 || k == 7) win_flush(w);
+            }
             if (w.live) {
                 store_block(lst + blk * 8, e);
                 if (blk * 8 + 7 == B.j1) win_mark_mu1(w);
@@ -748,7 +769,13 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 }
 
 // K3c: giant steps with per-lane refill and a pipelined lookup.
-__global__ void __launch_bounds__(256)
+#ifndef GIANT_THREADS
+#define GIANT_THREADS 128
+#endif
+#ifndef GIANT_MINB
+#define GIANT_MINB 5
+#endif
+__global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
 bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     __shared__ u32 hist[NROW_MAX * HIST_CAP];
     hist_zero(a, hist);
@@ -899,6 +926,17 @@ struct BsgsPlan {
     unsigned window_blocks, prep_blocks, giant_blocks;
 };
 
+// true if bsgs_prepare would (re)allocate scratch (the caller must then drain
+// every stream that may still use it)
+inline bool bsgs_needs_grow(const BsgsScratch &scr, u64 seg_len, u64 d_hi, int alpha_x16,
+                            int two_sided) {
+    const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided);
+    const size_t n = (size_t)seg_len;
+    return !scr.lists || n * (size_t)z.lcap > scr.lists_n ||
+           n * (size_t)z.nb * BKT > scr.tables_n || n > scr.brecs_n || n > scr.grecs_n ||
+           n > scr.bqueue_n || n > scr.gqueue_n;
+}
+
 inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
     const BsgsSizes z = bsgs_sizes(d_max, alpha, two_sided);
     return (size_t)4 * z.lcap + (size_t)64 * z.nb + sizeof(BabyRec) + sizeof(GiantRec) + 8;
@@ -948,7 +986,7 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
         per_sm < 1)
         return -4;
     pl.prep_blocks = (unsigned)(num_sms * per_sm);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_giant_kernel, BSGS_THREADS,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_giant_kernel, GIANT_THREADS,
                                                       0) != cudaSuccess ||
         per_sm < 1)
         return -4;
@@ -966,7 +1004,7 @@ inline int bsgs_launch_baby(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t 
 }
 
 inline int bsgs_launch_giant(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t s) {
-    bsgs_giant_kernel<<<pl.giant_blocks, BSGS_THREADS, 0, s>>>(a, pl.B, pl.o);
+    bsgs_giant_kernel<<<pl.giant_blocks, GIANT_THREADS, 0, s>>>(a, pl.B, pl.o);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 #endif  // __CUDACC__ (launch)

@@ -62,6 +62,7 @@ int main(int argc, char **argv) {
                 lst[1] = e1;
                 for (int j = 2; j < B.nw && w.live; j++) {
                     lst[j] = win_step(w);
+                    if ((j & 3) == 3) win_flush(w);
                     baby++;
                     if (j == B.j1 && w.live) win_mark_mu1(w);
                 }
