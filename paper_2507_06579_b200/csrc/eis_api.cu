@@ -208,6 +208,15 @@ bool want_bsgs(u64 d_lo) {
 // candidate index - i_first.  x_host/x_dev/n/buckets_dev (nullable) receive counts.
 int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u64 *x_dev,
               int n, u64 *buckets_dev, cudaStream_t s, int nrow = 2) {
+    // AUTO: a range that spans the crossover runs as two ranges (HALF below, BSGS
+    // at and above it)
+    if (g.mode == EIS_MODE_AUTO && cand_d(i_first) < g.crossover && cand_d(i_last) >= g.crossover) {
+        const u64 i_cross = (g.crossover - 5 + 7) / 8;     // least i with 8i + 5 >= crossover
+        if (int rc = run_range(i_first, i_cross - 1, flags_dev, x_host, x_dev, n, buckets_dev, s, nrow))
+            return rc;
+        return run_range(i_cross, i_last, flags_dev ? flags_dev + (i_cross - i_first) : nullptr,
+                         x_host, x_dev, n, buckets_dev, s, nrow);
+    }
     const int with_primes = nrow > 2;
     const u64 SEG = 1ull << g.segment_log2;
     const int n_small = primes_small();

@@ -118,6 +118,22 @@ def test_count_matches_oracle_and_flags(mode):
     assert np.array_equal(cD, oD) and np.array_equal(cE, oE)
 
 
+def test_auto_range_spanning_the_crossover():
+    """AUTO splits a range at the crossover (HALF below, BSGS at and above it):
+    flags and checkpoint counts across the split equal the oracle's."""
+    old = eis.get_option("crossover")
+    try:
+        eis.set_option("mode", eis.MODE_AUTO)
+        eis.set_option("crossover", 600_005)
+        _flags_equal(300_000, 900_000)
+        x = [400_000, 600_000, 600_005, 600_013, 800_000]
+        cD, cE = eis.count_window(300_000, x)
+        oD, oE = c_oracle.count_window(300_000, x, NTHREADS)
+        assert np.array_equal(cD, oD) and np.array_equal(cE, oE)
+    finally:
+        eis.set_option("crossover", old)
+
+
 def test_determinism(mode):
     a = eis.classify_range(10**8, 10**8 + 2_000_000)
     b = eis.classify_range(10**8, 10**8 + 2_000_000)
