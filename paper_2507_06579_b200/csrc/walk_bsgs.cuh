@@ -23,8 +23,8 @@
 // The store ("dictionary of ideals", l.549, l.607).  list[j] = Q_j | t_j << 20 for
 // the j-th baby entry (theta_{j+1} <-> (Q_j, P_j); t unreduced, < 2^12).  The
 // table is nb buckets of BKT = 16 slots (64 bytes, two DRAM sectors); slot =
-// (Q >> 2) | (j + 1) << 18 | (t_j mod 3) << 29, 0 = empty (Q = 2 mod 4 on
-// reduced ideals, so Q >> 2 identifies Q).  An entry goes to the first free
+// (Q >> 2) | (j + 1) << 18, 0 = empty (Q = 2 mod 4 on reduced ideals, so Q >> 2
+// identifies Q); t_j is read from the list on a match.  An entry goes to the first free
 // slot of bucket h(Q), else of the following buckets; slots fill in order, so
 // a lookup stops at the first empty slot.  P is not stored: on the principal
 // cycle P_j^2 = d - Q_{j-1} Q_j with P_j > 0 (rho), so a reduced (Q*, P*)
@@ -85,23 +85,24 @@ EIS_HD float two_sided_margin2(u64 d) {            // M in log2 units
 
 // ---------------------------------------------------------------- the store --
 EIS_HD u32 list_entry(u32 Q, u32 traw) { return Q | (traw << 20); }
-EIS_HD u32 slot_entry(u32 Q, u32 j, u32 t3) { return (Q >> 2) | ((j + 1) << 18) | (t3 << 29); }
-EIS_HD u32 slot_of(u32 e, u32 j) { return slot_entry(e & 0xFFFFFu, j, mod3_small(e >> 20)); }
-EIS_HD u32 store_bucket(u32 Q, u32 nb) {           // multiply-shift hash onto [0, nb)
-    return (u32)(((u64)(Q * 0x9E3779B1u) * nb) >> 32);
+// key = Q >> 2 identifies Q (Q = 2 mod 4 on reduced ideals)
+EIS_HD u32 entry_key(u32 e) { return (e & 0xFFFFFu) >> 2; }
+EIS_HD u32 slot_entry(u32 key, u32 j) { return key | ((j + 1) << 18); }
+EIS_HD u32 store_bucket(u32 key, u32 nb) {         // multiply-shift hash onto [0, nb)
+    return (u32)(((u64)(key * 0x9E3779B1u) * nb) >> 32);
 }
 EIS_HD u32 next_bucket(u32 b, u32 nb) { return b + 1 == nb ? 0u : b + 1; }
 
 // host/emulation build: sequential insertion into a zeroed table
 EIS_HD void store_build_seq(u32 *tab, u32 nb, const u32 *list, u32 n) {
     for (u32 j = 0; j < n; j++) {
-        const u32 e = list[j], Q = e & 0xFFFFFu;
-        u32 b = store_bucket(Q, nb);
+        const u32 e = list[j], key = entry_key(e);
+        u32 b = store_bucket(key, nb);
         for (;;) {
             u32 i = 0;
             while (i < (u32)BKT && tab[b * BKT + i] != 0) i++;
             if (i < (u32)BKT) {
-                tab[b * BKT + i] = slot_of(e, j);
+                tab[b * BKT + i] = slot_entry(key, j);
                 break;
             }
             b = next_bucket(b, nb);
@@ -127,7 +128,7 @@ EIS_HD void load_bucket(const u32 *tab, u32 b, Probe &p) {
 
 EIS_HD Probe store_probe(const u32 *tab, u32 nb, u32 Q) {
     Probe p;
-    load_bucket(tab, store_bucket(Q, nb), p);
+    load_bucket(tab, store_bucket(Q >> 2, nb), p);
     return p;
 }
 
@@ -182,7 +183,7 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
             const u32 Qprev = jj ? (list[jj - 1] & 0xFFFFFu) : 0u;
             const int k = match_kind(d, Q, P, s, jj, Qprev);
             if (k != HIT_NONE) {
-                t3 = e >> 29;
+                t3 = jj ? mod3(list[jj] >> 20) : 0u;      // t(theta), from the list
                 j = jj;
                 return k;
             }
@@ -566,43 +567,49 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
                                             u32 *cnt, u32 *__restrict__ dst) {
     const int lane = threadIdx.x & 31;
     // the lists come back from DRAM (far more of them are in flight than L2
-    // holds): loads run one group of 256 entries (8 per lane) ahead
-    constexpr int G = 8;
-    u32 nx[G];
+    // holds): 16-byte loads run one group of 256 entries (2 per lane) ahead;
+    // lists are padded to lcap (a multiple of 32), so the loads stay in bounds
+    const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
+    const u32 n4 = (n + 3) >> 2;
+    uint4 nx[2];
 #pragma unroll
-    for (int k = 0; k < G; k++) {
-        const u32 jn = (u32)(32 * k + lane);
-        nx[k] = jn < n ? lst[jn] : 0u;
+    for (int k = 0; k < 2; k++) {
+        const u32 i4 = (u32)(32 * k + lane);
+        nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
     }
-    for (u32 jb = 0; jb < n; jb += 32 * G) {
-        u32 cur[G];
+    for (u32 jb = 0; jb < n; jb += 256) {
+        uint4 cur[2];
 #pragma unroll
-        for (int k = 0; k < G; k++) {
+        for (int k = 0; k < 2; k++) {
             cur[k] = nx[k];
-            const u32 jn = jb + 32 * (G + k) + lane;
-            nx[k] = jn < n ? lst[jn] : 0u;
+            const u32 i4 = jb / 4 + (u32)(64 + 32 * k + lane);
+            nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int k = 0; k < G; k++) {
-            const u32 j = jb + 32 * k + lane;
-            const u32 e = cur[k];
-            const u32 sv = slot_of(e, j);
-            u32 b = store_bucket(e & 0xFFFFFu, nb);
-            // one attempt; a full bucket (rare at load 0.62) sends the entry onward
-            // in a warp-uniform slow loop
-            bool ovf = false;
-            if (j < n) {
-                const u32 pos = atomicAdd(&cnt[b], 1u);
-                if (pos < (u32)BKT) tab[b * BKT + pos] = sv;
-                else ovf = true;
-            }
-            while (__any_sync(FULL_MASK, ovf)) {
-                if (ovf) {
-                    b = next_bucket(b, nb);
+        for (int k = 0; k < 2; k++) {
+#pragma unroll
+            for (int w = 0; w < 4; w++) {
+                const u32 j = jb + 128 * k + 4 * lane + w;
+                const u32 e = w == 0 ? cur[k].x : (w == 1 ? cur[k].y : (w == 2 ? cur[k].z : cur[k].w));
+                const u32 key = entry_key(e);
+                const u32 sv = slot_entry(key, j);
+                u32 b = store_bucket(key, nb);
+                // one attempt; a full bucket (rare at load 0.62) sends the entry onward
+                // in a warp-uniform slow loop
+                bool ovf = false;
+                if (j < n) {
                     const u32 pos = atomicAdd(&cnt[b], 1u);
-                    if (pos < (u32)BKT) {
-                        tab[b * BKT + pos] = sv;
-                        ovf = false;
+                    if (pos < (u32)BKT) tab[b * BKT + pos] = sv;
+                    else ovf = true;
+                }
+                while (__any_sync(FULL_MASK, ovf)) {
+                    if (ovf) {
+                        b = next_bucket(b, nb);
+                        const u32 pos = atomicAdd(&cnt[b], 1u);
+                        if (pos < (u32)BKT) {
+                            tab[b * BKT + pos] = sv;
+                            ovf = false;
+                        }
                     }
                 }
             }
