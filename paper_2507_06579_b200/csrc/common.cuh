@@ -11,6 +11,7 @@ typedef int64_t i64;
 typedef uint32_t u32;
 typedef int32_t i32;
 typedef uint8_t u8;
+typedef uint16_t u16;
 
 #define FULL_MASK 0xffffffffu
 

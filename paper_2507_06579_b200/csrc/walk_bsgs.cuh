@@ -49,7 +49,10 @@
 constexpr float LN2F = 0.69314718f;
 constexpr float GUARD_LOG2 = 1.0f / LN2F;    // "log mu'_k - log theta >= 1" in log2 units
 constexpr int BKT = 16;                       // slots per table bucket (64 bytes)
-constexpr float BKT_LOAD = 0.62f;             // table load factor
+#ifndef BKT_LOAD_X100
+#define BKT_LOAD_X100 62
+#endif
+constexpr float BKT_LOAD = BKT_LOAD_X100 / 100.f;   // table load factor
 
 enum LanePhase : u32 { PH_IDLE = 0, PH_BABY = 1, PH_GIANT = 2, PH_HALF = 3, PH_DONE = 4 };
 
@@ -626,7 +629,10 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(256)
+#ifndef WINDOW_MINB
+#define WINDOW_MINB 5
+#endif
+__global__ void __launch_bounds__(256, WINDOW_MINB)
 bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     extern __shared__ u32 smem[];
     __shared__ u32 hist[NROW_MAX * HIST_CAP];
