@@ -92,7 +92,11 @@ EIS_HD u32 list_entry(u32 Q, u32 traw) { return Q | (traw << 20); }
 EIS_HD u32 entry_key(u32 e) { return (e & 0xFFFFFu) >> 2; }
 EIS_HD u32 slot_entry(u32 key, u32 j) { return key | ((j + 1) << 18); }
 EIS_HD u32 store_bucket(u32 key, u32 nb) {         // multiply-shift hash onto [0, nb)
+#ifdef __CUDA_ARCH__
+    return __umulhi(key * 0x9E3779B1u, nb);
+#else
     return (u32)(((u64)(key * 0x9E3779B1u) * nb) >> 32);
+#endif
 }
 EIS_HD u32 next_bucket(u32 b, u32 nb) { return b + 1 == nb ? 0u : b + 1; }
 
@@ -564,11 +568,22 @@ __device__ __forceinline__ void store_block(u32 *dst, const u32 (&e)[8]) {
     reinterpret_cast<uint4 *>(dst)[1] = make_uint4(e[4], e[5], e[6], e[7]);
 }
 
+__device__ __forceinline__ u32 smem_atom_inc(u32 addr) {
+    u32 old;
+    asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(addr) : "memory");
+    return old;
+}
+__device__ __forceinline__ void smem_st(u32 addr, u32 v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // One store, built by the whole warp in shared memory (tab: nb * BKT slots, cnt:
 // nb fill counters, both zero on entry and on exit) and written to dst.
 __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, u32 nb, u32 *tab,
                                             u32 *cnt, u32 *__restrict__ dst) {
     const int lane = threadIdx.x & 31;
+    const u32 tab_s = (u32)__cvta_generic_to_shared(tab);   // shared-window addresses
+    const u32 cnt_s = (u32)__cvta_generic_to_shared(cnt);
     // the lists come back from DRAM (far more of them are in flight than L2
     // holds): 16-byte loads run one group of 256 entries (2 per lane) ahead;
     // lists are padded to lcap (a multiple of 32), so the loads stay in bounds
@@ -599,19 +614,19 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
                 u32 b = store_bucket(key, nb);
                 // one attempt; a full bucket (rare at load 0.62) sends the entry onward
                 // in a warp-uniform slow loop
-                bool ovf = false;
+                u32 ovf = 0;
                 if (j < n) {
-                    const u32 pos = atomicAdd(&cnt[b], 1u);
-                    if (pos < (u32)BKT) tab[b * BKT + pos] = sv;
-                    else ovf = true;
+                    const u32 pos = smem_atom_inc(cnt_s + 4 * b);
+                    if (pos < (u32)BKT) smem_st(tab_s + 4 * (b * BKT + pos), sv);
+                    else ovf = 1;
                 }
                 while (__any_sync(FULL_MASK, ovf)) {
                     if (ovf) {
                         b = next_bucket(b, nb);
-                        const u32 pos = atomicAdd(&cnt[b], 1u);
+                        const u32 pos = smem_atom_inc(cnt_s + 4 * b);
                         if (pos < (u32)BKT) {
-                            tab[b * BKT + pos] = sv;
-                            ovf = false;
+                            smem_st(tab_s + 4 * (b * BKT + pos), sv);
+                            ovf = 0;
                         }
                     }
                 }
