@@ -64,6 +64,7 @@ struct Ctx {
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
     int threads = 256;
     int giant_ctas = 0;
+    int window_ctas = 0;             // BSGS window kernel CTAs per SM (0 = occupancy maximum)
     int half_ksteps = 0;             // 0: chosen per segment from d
     int two_sided = 1;               // BSGS: two-sided window (R35); 0 = paper's Alg. 1
     // instrumentation of the last call
@@ -306,7 +307,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
                 CUDA_TRY(cudaStreamSynchronize(s));
             }
             int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.giant_ctas, g.two_sided, bf.bsgs,
-                                  bf.ctr + 2);
+                                  bf.ctr + 2, g.window_ctas);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -508,6 +509,7 @@ void eis_finalize(void) {
     fresh.segment_log2 = g.segment_log2;
     fresh.blocks_per_sm = g.blocks_per_sm;
     fresh.giant_ctas = g.giant_ctas;
+    fresh.window_ctas = g.window_ctas;
     fresh.half_ksteps = g.half_ksteps;
     fresh.two_sided = g.two_sided;
     g = fresh;
@@ -530,6 +532,9 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "segment_log2") {
         if (v < 18 || v > 31) return fail(EIS_EINVAL, "segment_log2 must be in [18, 31]");
         g.segment_log2 = (int)v;
+    } else if (k == "window_ctas") {
+        if (v < 0 || v > 32) return fail(EIS_EINVAL, "window_ctas must be in [0, 32]");
+        g.window_ctas = (int)v;
     } else if (k == "giant_ctas") {
         if (v < 0 || v > 32) return fail(EIS_EINVAL, "giant_ctas must be in [0, 32]");
         g.giant_ctas = (int)v;
@@ -558,6 +563,7 @@ int64_t eis_get_option(const char *key) {
     if (k == "segment_log2") return g.segment_log2;
     if (k == "blocks_per_sm") return g.blocks_per_sm;
     if (k == "giant_ctas") return g.giant_ctas;
+    if (k == "window_ctas") return g.window_ctas;
     if (k == "half_ksteps") return g.half_ksteps;
     if (k == "two_sided") return g.two_sided;
     return fail(EIS_EINVAL, "unknown option '%s'", key);

@@ -974,7 +974,8 @@ inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
 // Size one segment buffer (seg_len candidates bound the survivors) and choose
 // the launch shapes.  ctr: 4 device counters (zeroed by bsgs_launch_window).
 inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
-                        int giant_ctas, int two_sided, BsgsScratch &scr, u32 *ctr) {
+                        int giant_ctas, int two_sided, BsgsScratch &scr, u32 *ctr,
+                        int window_ctas = 0) {
     BsgsArgs &B = pl.B;
     const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided);
     B.nw = z.nw;
@@ -1008,7 +1009,7 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
                                                       pl.window_smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
-    pl.window_blocks = (unsigned)(num_sms * per_sm);
+    pl.window_blocks = (unsigned)(num_sms * (window_ctas > 0 ? std::min(window_ctas, per_sm) : per_sm));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_prep_kernel, BSGS_THREADS,
                                                       0) != cudaSuccess ||
         per_sm < 1)
