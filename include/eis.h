@@ -97,6 +97,7 @@ EIS_API const char *eis_last_error(void);
  *  "blocks_per_sm" HALF walk kernel CTAs per SM
  *  "giant_ctas"    BSGS giant kernel CTAs per SM (0 = occupancy maximum)
  *  "window_ctas"   BSGS window kernel CTAs per SM (0 = occupancy maximum)
+ *  "bsgs_gb"       BSGS store memory per segment buffer in GiB (two buffers), [1, 64]
  *  "half_ksteps"   HALF walk: rho steps per lane between refills (0 = auto, 18/36/72/144)
  *  "two_sided"     BSGS: 1 (default) = the store is also matched against conjugates and
  *                  the giant stride is mu_1^2 (R35); 0 = the paper's one-sided
