@@ -603,30 +603,37 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
             const u32 i4 = jb / 4 + (u32)(64 + 32 * k + lane);
             nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
         }
+        // first attempts for the group's 8 entries per lane back to back (their
+        // atomics overlap), then one warp-uniform loop for full buckets (rare)
+        u32 ovf = 0;                                     // bit i: entry i still to place
+        u32 bb[8], sv[8];
 #pragma unroll
         for (int k = 0; k < 2; k++) {
 #pragma unroll
             for (int w = 0; w < 4; w++) {
+                const int i = 4 * k + w;
                 const u32 j = jb + 128 * k + 4 * lane + w;
                 const u32 e = w == 0 ? cur[k].x : (w == 1 ? cur[k].y : (w == 2 ? cur[k].z : cur[k].w));
                 const u32 key = entry_key(e);
-                const u32 sv = slot_entry(key, j);
-                u32 b = store_bucket(key, nb);
-                // one attempt; a full bucket (rare at load 0.62) sends the entry onward
-                // in a warp-uniform slow loop
-                u32 ovf = 0;
+                sv[i] = slot_entry(key, j);
+                bb[i] = store_bucket(key, nb);
                 if (j < n) {
-                    const u32 pos = smem_atom_inc(cnt_s + 4 * b);
-                    if (pos < (u32)BKT) smem_st(tab_s + 4 * (b * BKT + pos), sv);
-                    else ovf = 1;
+                    const u32 pos = smem_atom_inc(cnt_s + 4 * bb[i]);
+                    if (pos < (u32)BKT) smem_st(tab_s + 4 * (bb[i] * BKT + pos), sv[i]);
+                    else ovf |= 1u << i;
                 }
-                while (__any_sync(FULL_MASK, ovf)) {
-                    if (ovf) {
-                        b = next_bucket(b, nb);
-                        const u32 pos = smem_atom_inc(cnt_s + 4 * b);
+            }
+        }
+        while (__any_sync(FULL_MASK, ovf)) {
+            if (ovf) {
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    if (ovf & (1u << i)) {
+                        bb[i] = next_bucket(bb[i], nb);
+                        const u32 pos = smem_atom_inc(cnt_s + 4 * bb[i]);
                         if (pos < (u32)BKT) {
-                            smem_st(tab_s + 4 * (b * BKT + pos), sv);
-                            ovf = 0;
+                            smem_st(tab_s + 4 * (bb[i] * BKT + pos), sv[i]);
+                            ovf &= ~(1u << i);
                         }
                     }
                 }
