@@ -118,6 +118,24 @@ def test_count_matches_oracle_and_flags(mode):
     assert np.array_equal(cD, oD) and np.array_equal(cE, oE)
 
 
+@pytest.mark.parametrize("opts", [{"two_sided": 0}, {"bsgs_gb": 1}, {"alpha_x16": 8},
+                                  {"alpha_x16": 64, "two_sided": 0}])
+def test_bsgs_options_do_not_change_results(opts):
+    """BSGS with the paper's one-sided Alg. 1 (two_sided=0), tiny store memory
+    (many segments), and extreme windows: flags equal the oracle's (R6, R29, R35)."""
+    old = {k: eis.get_option(k) for k in opts}
+    try:
+        eis.set_option("mode", eis.MODE_BSGS)
+        for k, v in opts.items():
+            eis.set_option(k, v)
+        _flags_equal(10**9 - 20_003, 10**9 + 7)
+        _flags_equal(10**10 - 8_001, 10**10)
+    finally:
+        for k, v in old.items():
+            eis.set_option(k, v)
+        eis.set_option("mode", eis.MODE_AUTO)
+
+
 def test_auto_range_spanning_the_crossover():
     """AUTO splits a range at the crossover (HALF below, BSGS at and above it):
     flags and checkpoint counts across the split equal the oracle's."""
