@@ -810,54 +810,99 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #ifndef GIANT_MINB
 #define GIANT_MINB 5
 #endif
+constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
 bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    // per-warp ring of resume records: refills (about one per warp iteration)
+    // read shared memory; the queue and the records are fetched 32 at a time
+    __shared__ GiantRec stash[GIANT_THREADS / 32][STASH];
+    __shared__ u32 sidx[GIANT_THREADS / 32][STASH];
+    __shared__ uint4 pbuf[GIANT_THREADS][4];           // the bucket being probed, per lane
     hist_zero(a, hist);
     __syncthreads();
 
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 nq = o.ctr[2];
     const u32 *tab = nullptr, *list = nullptr;
     GiantLane g;
     g.phase = PH_IDLE;
     u32 off = 0;
     bool exhausted = false;
+    u32 head = 0, tail = 0;                            // warp-uniform ring positions
+    bool qdone = false;                                // the queue is drained
     u64 baby = 0, giant = 0, red = 0, done = 0, fb = 0;
     u32 err = 0;
 
     for (;;) {
         const u32 need = __ballot_sync(FULL_MASK, g.phase == PH_IDLE && !exhausted);
         if (need) {
-            const int leader = __ffs(need) - 1;
-            u32 base = 0;
-            if (lane == leader) base = atomicAdd(&o.ctr[3], (u32)__popc(need));
-            base = __shfl_sync(FULL_MASK, base, leader);
-            if (g.phase == PH_IDLE && !exhausted) {
-                const u32 qi = base + __popc(need & lanemask_lt());
-                if (qi < nq) {
+            const u32 k = (u32)__popc(need);
+            if (tail - head < k && !qdone) {           // fill the ring's free slots
+                const u32 want = STASH - (tail - head);     // <= 32
+                u32 base = 0;
+                if (lane == 0) base = atomicAdd(&o.ctr[3], want);
+                base = __shfl_sync(FULL_MASK, base, 0);
+                const u32 qi = base + (u32)lane;
+                if ((u32)lane < want && qi < nq) {
                     const u32 idx = __ldg(o.gqueue + qi);
-                    const GiantRec r = o.grecs[idx];
-                    off = r.off;                          // (with the prime bit)
-                    giant_unpack(g, r, cand_d(a.i0 + (off & ~PRIME_BIT)));
+                    const u32 sl = (tail + (u32)lane) & (STASH - 1);
+                    stash[wid][sl] = o.grecs[idx];
+                    sidx[wid][sl] = idx;
+                }
+                const u32 got = base >= nq ? 0u : min(want, nq - base);
+                if (got < want) qdone = true;
+                tail += got;
+                __syncwarp();
+            }
+            const u32 avail = tail - head;
+            if (g.phase == PH_IDLE && !exhausted) {
+                const u32 r = (u32)__popc(need & lanemask_lt());
+                if (r < avail) {
+                    const u32 sl = (head + r) & (STASH - 1);
+                    const u32 idx = sidx[wid][sl];
+                    const GiantRec rec = stash[wid][sl];
+                    off = rec.off;                        // (with the prime bit)
+                    giant_unpack(g, rec, cand_d(a.i0 + (off & ~PRIME_BIT)));
                     tab = o.tables + (u64)idx * ((u64)B.nb * BKT);
                     list = o.lists + (u64)idx * B.lcap;
                 } else {
-                    exhausted = true;
+                    exhausted = true;                     // (only when qdone)
                 }
             }
+            head += min(k, avail);
+            __syncwarp();
         }
         if (__all_sync(FULL_MASK, exhausted && g.phase == PH_IDLE)) break;
         const u32 gmask = __ballot_sync(FULL_MASK, g.phase == PH_GIANT);
         if (g.phase == PH_GIANT) {
             // software pipeline: probe mu'_k (refills start with mu'_2, not yet
             // probed) while computing mu'_{k+1}
+            // probed while computing mu'_{k+1}; the bucket is copied to shared
+            // memory asynchronously (cp.async), so no registers wait across the
+            // composition and the compiler cannot sink the load to its use
             const u32 pQ = g.Qc, pP = g.Pc, pt = g.tc;
             const float pdist = g.distc;
-            const Probe pr = store_probe(tab, B.nb, pQ);
+            const u32 pb = store_bucket(pQ >> 2, (u32)B.nb);
+            {
+                const u32 *src = tab + (size_t)pb * BKT;
+                const u32 dst = (u32)__cvta_generic_to_shared(&pbuf[threadIdx.x][0]);
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q),
+                                 "l"(src + 4 * q) : "memory");
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
             const GiantInfo gi = giant_advance(g, B, &err, gmask);
             giant++;
             red += gi.nred;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            Probe pr;
+            pr.b = pb;
+            pr.g0 = pbuf[threadIdx.x][0];
+            pr.g1 = pbuf[threadIdx.x][1];
+            pr.g2 = pbuf[threadIdx.x][2];
+            pr.g3 = pbuf[threadIdx.x][3];
             u32 te, j;
             const int kind = store_resolve(tab, list, B.nb, pr, g.d, (u32)g.s, pQ, pP, te, j);
             warp_reconverge(gmask);
