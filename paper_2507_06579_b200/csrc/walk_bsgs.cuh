@@ -144,15 +144,15 @@ EIS_HD Probe store_probe(const u32 *tab, u32 nb, u32 Q) {
 enum HitKind : int { HIT_NONE = 0, HIT_DIRECT = 1, HIT_CONJ = 2 };
 
 // P-bar: the canonical representative in (s - Q, s] of -P mod Q
-EIS_HD u32 conj_P(u32 Q, u32 P, u32 s) {
-    const u32 r = (s + P) % Q;
-    return s - r;
+EIS_HD u32 conj_P(u32 Q, u32 P, u32 s) {     // = floor((s + P)/Q) Q - P (a rho step's P)
+    const float q = ffloor_div_pos((float)(s + P), (float)Q);   // exact: s + P, Q < 2^21
+    return (u32)q * Q - P;
 }
 
 // Entry jj >= 1 holds (Q_j, P_j) with P_j^2 = d - Q_{j-1} Q_j, P_j > 0 on reduced
 // ideals, so Q_{j-1} identifies P_j; entry 0 is (2, P_1) = O, the only reduced
 // ideal with Q = 2 (self-conjugate).
-EIS_HD int match_kind(u64 d, u32 Q, u32 P, u32 s, u32 jj, u32 Qprev) {
+EIS_HD_COLD int match_kind(u64 d, u32 Q, u32 P, u32 s, u32 jj, u32 Qprev) {   // (rare)
     if (jj == 0) return HIT_DIRECT;
     const u64 nrm = d - (u64)Qprev * Q;
     if ((u64)P * P == nrm) return HIT_DIRECT;
@@ -366,7 +366,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
                                       B.plain_th, err, wmask);
     warp_reconverge(wmask);
     gi.kind = c.kind;
-    u32 t = mod3(g.t1 + g.tc + 3u - c.tg);       // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
+    u32 t = mod3_small(g.t1 + g.tc + 3u - c.tg);   // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
     float dist = g.dist1 + g.distc - c.lg;
     i64 Q = c.Q, P = c.P;                        // P canonical in (s - Q, s]
     u32 nred = 0;
@@ -384,7 +384,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
             const i64 nQ = d - Pni * Pni;
             const double Qn = rint((double)nQ * rQ);
             if ((i64)Qn * (i64)Qd != nQ) *err += 1;
-            t = mod3(t + 1u + (u32)((Pni >> 1) & 1));
+            t = mod3_small(t + 1u + (u32)((Pni >> 1) & 1));
             dist += log2_approx((float)fabs(Pn + g.sqrtd)) - log2_approx((float)Qd);
             Qd = fabs(Qn);
             rQ = rcp64(Qd);
