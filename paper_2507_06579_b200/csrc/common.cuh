@@ -166,6 +166,12 @@ __device__ __forceinline__ int bucket_of(const u64 *x, int lo, int hi, u64 d) {
     return lo;
 }
 
+// shared-memory words of a walk kernel's histogram (dynamic shared memory, a
+// multiple of 4 so that what follows stays 16-byte aligned)
+inline __host__ __device__ u32 hist_words(const WalkArgs &a) {
+    return a.ckpt ? ((u32)(a.nrow * a.nb) + 3u) & ~3u : 0u;
+}
+
 #ifdef __CUDACC__
 __device__ __forceinline__ void hist_zero(const WalkArgs &a, u32 *hist) {
     for (int i = threadIdx.x; i < a.nrow * a.nb; i += blockDim.x) hist[i] = 0;

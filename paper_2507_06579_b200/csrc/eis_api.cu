@@ -309,7 +309,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
                 CUDA_TRY(cudaStreamSynchronize(s));
             }
             int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.giant_ctas, g.two_sided, bf.bsgs,
-                                  bf.ctr + 2, g.window_ctas);
+                                  bf.ctr + 2, g.window_ctas, hist_words(a));
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -340,12 +340,13 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
                 const double exp_steps = 0.07 * std::sqrt((double)cand_d(seg));
                 ks = exp_steps >= 8 * 144 ? 144 : exp_steps >= 8 * 72 ? 72 : exp_steps >= 8 * 36 ? 36 : 18;
             }
+            const size_t hb = (size_t)hist_words(a) * sizeof(u32);
             CUDA_TRY(cudaEventRecord(kev_next(e0), s));
             switch (ks) {
-                case 18: walk_half_kernel<18><<<wblocks, 256, 0, s>>>(a); break;
-                case 72: walk_half_kernel<72><<<wblocks, 256, 0, s>>>(a); break;
-                case 144: walk_half_kernel<144><<<wblocks, 256, 0, s>>>(a); break;
-                default: walk_half_kernel<36><<<wblocks, 256, 0, s>>>(a); break;
+                case 18: walk_half_kernel<18><<<wblocks, 256, hb, s>>>(a); break;
+                case 72: walk_half_kernel<72><<<wblocks, 256, hb, s>>>(a); break;
+                case 144: walk_half_kernel<144><<<wblocks, 256, hb, s>>>(a); break;
+                default: walk_half_kernel<36><<<wblocks, 256, hb, s>>>(a); break;
             }
             CUDA_TRY(cudaGetLastError());
             CUDA_TRY(cudaEventRecord(kev_next(e1), s));

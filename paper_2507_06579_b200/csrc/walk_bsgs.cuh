@@ -656,12 +656,12 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
 #endif
 __global__ void __launch_bounds__(256, WINDOW_MINB)
 bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
-    extern __shared__ u32 smem[];
-    __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    extern __shared__ u32 smem[];                       // histogram, then per-warp tables
+    u32 *hist = smem;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 nb = (u32)B.nb;
     const u32 wstride = window_smem_words(nb);               // 16-byte aligned per warp
-    u32 *tab = smem + (size_t)wid * wstride;
+    u32 *tab = smem + hist_words(a) + (size_t)wid * wstride;
     u32 *cnt = tab + nb * BKT;
     hist_zero(a, hist);
     for (u32 i = lane; i < wstride; i += 32) tab[i] = 0;
@@ -738,7 +738,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 // looked up here and mu''_2 = mu''_1^2 (NUDUPL again) taken in lockstep too.
 __global__ void __launch_bounds__(256)
 bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
-    __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    extern __shared__ u32 hist[];                       // hist_words(a)
     hist_zero(a, hist);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -813,7 +813,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
 bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
-    __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    extern __shared__ u32 hist[];                       // hist_words(a)
     // per-warp ring of resume records: refills (about one per warp iteration)
     // read shared memory; the queue and the records are fetched 32 at a time
     __shared__ GiantRec stash[GIANT_THREADS / 32][STASH];
@@ -1002,7 +1002,7 @@ inline int bsgs_grow(T *&p, size_t &cap, size_t n) {
 struct BsgsPlan {
     BsgsArgs B;
     BsgsOut o;
-    size_t window_smem;
+    size_t window_smem, hist_smem;
     unsigned window_blocks, prep_blocks, giant_blocks;
 };
 
@@ -1027,7 +1027,7 @@ inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
 // the launch shapes.  ctr: 4 device counters (zeroed by bsgs_launch_window).
 inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
                         int giant_ctas, int two_sided, BsgsScratch &scr, u32 *ctr,
-                        int window_ctas = 0) {
+                        int window_ctas, u32 hist_w) {
     BsgsArgs &B = pl.B;
     const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided);
     B.nw = z.nw;
@@ -1053,7 +1053,9 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     o.gqueue = scr.gqueue;
     o.ctr = ctr;
     int per_sm = 0;
-    pl.window_smem = (size_t)(BSGS_THREADS / 32) * window_smem_words((u32)z.nb) * sizeof(u32);
+    pl.hist_smem = (size_t)hist_w * sizeof(u32);
+    pl.window_smem =
+        pl.hist_smem + (size_t)(BSGS_THREADS / 32) * window_smem_words((u32)z.nb) * sizeof(u32);
     if (cudaFuncSetAttribute(bsgs_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pl.window_smem) != cudaSuccess)
         return -4;
@@ -1063,12 +1065,12 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
         return -4;
     pl.window_blocks = (unsigned)(num_sms * (window_ctas > 0 ? std::min(window_ctas, per_sm) : per_sm));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_prep_kernel, BSGS_THREADS,
-                                                      0) != cudaSuccess ||
+                                                      pl.hist_smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
     pl.prep_blocks = (unsigned)(num_sms * per_sm);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_giant_kernel, GIANT_THREADS,
-                                                      0) != cudaSuccess ||
+                                                      pl.hist_smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
     pl.giant_blocks = (unsigned)(num_sms * (giant_ctas > 0 ? std::min(giant_ctas, per_sm) : per_sm));
@@ -1080,12 +1082,12 @@ inline int bsgs_launch_baby(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t 
     if (cudaMemsetAsync(pl.o.ctr, 0, 4 * sizeof(u32), s) != cudaSuccess) return -4;
     bsgs_window_kernel<<<pl.window_blocks, BSGS_THREADS, pl.window_smem, s>>>(a, pl.B, pl.o);
     if (cudaGetLastError() != cudaSuccess) return -4;
-    bsgs_prep_kernel<<<pl.prep_blocks, BSGS_THREADS, 0, s>>>(a, pl.B, pl.o);
+    bsgs_prep_kernel<<<pl.prep_blocks, BSGS_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
 inline int bsgs_launch_giant(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t s) {
-    bsgs_giant_kernel<<<pl.giant_blocks, GIANT_THREADS, 0, s>>>(a, pl.B, pl.o);
+    bsgs_giant_kernel<<<pl.giant_blocks, GIANT_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 #endif  // __CUDACC__ (launch)

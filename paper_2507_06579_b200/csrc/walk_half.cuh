@@ -143,7 +143,7 @@ EIS_HD u32 half_step_cap(u32 s) { return 48u * s + 64u; }
 template <int KSTEPS>
 __global__ void __launch_bounds__(256)
 walk_half_kernel(WalkArgs a) {
-    __shared__ u32 hist[NROW_MAX * HIST_CAP];
+    extern __shared__ u32 hist[];                  // hist_words(a)
     hist_zero(a, hist);
     __syncthreads();
 
