@@ -55,9 +55,9 @@ struct Ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // options
     int mode = EIS_MODE_AUTO;
-    u64 crossover = 8000000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
-                                     // HALF 2.0x faster at 1e9, BSGS 1.02x at 1e10, 1.35x
-                                     // at 3e10, 1.76x at 1e11)
+    u64 crossover = 4000000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
+                                     // HALF 1.08x faster at 3e9, BSGS 1.09x at 5e9, 1.27x
+                                     // at 1e10, 2.2x at 1e11)
     int alpha_x16 = 28;              // BSGS baby window W = alpha * d^(1/4) (best at 1e10,
                                      // within 1% of the best at 1e11)
     int segment_log2 = 25;
