@@ -22,17 +22,39 @@ import torch.distributed as dist
 from . import count_buckets_dev, prefix_dev
 
 
+# Measured per-d device cost of the default (AUTO) path on one B200:
+# HALF below the crossover, rate ~ 2.68e8 (1e10/d)^(1/2) d/s; BSGS at and above
+# it, rate ~ 3.41e8 (1e10/d)^0.24 d/s.  Only the shape matters for splitting.
+AUTO_CROSSOVER = 4_000_000_000
+
+
+def auto_cost_density(d: np.ndarray) -> np.ndarray:
+    """Relative device time per candidate at d under EIS_MODE_AUTO."""
+    d = np.maximum(np.asarray(d, dtype=np.float64), 1.0)
+    half = (d / 1e10) ** 0.5 / 2.68e8
+    bsgs = (d / 1e10) ** 0.24 / 3.41e8
+    return np.where(d < AUTO_CROSSOVER, half, bsgs)
+
+
 def shard_bounds(lo: int, hi: int, world: int, rank: int, balance: str = "flat") -> tuple[int, int]:
-    """Contiguous shard (a, b] of (lo, hi] for ``rank``.
+    """Contiguous shard (a, b] of (lo, hi] for ``rank`` (SURVEY.md 8(e)).
 
     balance="flat": equal widths (per-d cost is flat inside a window near a
     fixed scale).  balance="prefix": equal cost for a prefix (0, X] where the
     per-d cost grows like d^(1/4), so the cumulative cost grows like x^(5/4):
-    cut points x_g = X (g/G)^(4/5).  Boundaries are rounded
-    to multiples of 8 (never = 5 mod 8), so no candidate is split.
+    cut points x_g = X (g/G)^(4/5).  balance="auto": equal cost under the
+    measured cost of the AUTO path (HALF ~ d^(1/2) below 4e9, BSGS ~ d^0.24
+    above), integrated numerically over (lo, hi].  Boundaries are rounded to
+    multiples of 8 (never = 5 mod 8), so no candidate is split.
     """
     if world <= 1:
         return lo, hi
+    cum = None
+    if balance == "auto":
+        xs = np.linspace(lo, hi, 4097)
+        c = auto_cost_density(np.maximum(xs, 1.0))
+        cum = np.concatenate([[0.0], np.cumsum(0.5 * (c[1:] + c[:-1]) * np.diff(xs))])
+        cum /= cum[-1]
 
     def cut(g: int) -> int:
         if g <= 0:
@@ -41,6 +63,8 @@ def shard_bounds(lo: int, hi: int, world: int, rank: int, balance: str = "flat")
             return hi
         if balance == "prefix":
             v = lo + int((hi - lo) * (g / world) ** 0.8)
+        elif balance == "auto":
+            v = int(np.interp(g / world, cum, xs))
         else:
             v = lo + (hi - lo) * g // world
         return min(hi, max(lo, v - v % 8))
@@ -57,7 +81,7 @@ def allreduce_buckets(buckets: torch.Tensor, group: Optional[dist.ProcessGroup] 
 
 
 def count_window_distributed(lo: int, x, group: Optional[dist.ProcessGroup] = None,
-                             balance: str = "flat") -> tuple[np.ndarray, np.ndarray]:
+                             balance: str = "auto") -> tuple[np.ndarray, np.ndarray]:
     """cnt_D[i], cnt_E[i] over lo < d <= x[i], computed by all ranks of ``group``
     (one GPU each, the current CUDA device).  Every rank passes the same (lo, x)
     and receives the full result."""

@@ -56,7 +56,7 @@ def _worker(rank, world, port, lo, x, balance, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,balance", [(2, "flat"), (2, "prefix"), (3, "prefix")])
+@pytest.mark.parametrize("world,balance", [(2, "flat"), (2, "prefix"), (3, "prefix"), (3, "auto")])
 def test_sharded_allreduce_matches_single_process(world, balance):
     lo = 0 if balance == "prefix" else 123_457
     x = np.array([200_000, 350_001, 500_000, 777_777], dtype=np.uint64)
@@ -90,7 +90,7 @@ def test_sharded_allreduce_matches_single_process(world, balance):
 
 def test_shard_bounds_properties():
     for world in (1, 2, 4, 8):
-        for balance in ("flat", "prefix"):
+        for balance in ("flat", "prefix", "auto"):
             lo, hi = 9 * 10**9, 10**10
             cuts = [shard_bounds(lo, hi, world, r, balance) for r in range(world)]
             assert cuts[0][0] == lo and cuts[-1][1] == hi
@@ -100,3 +100,20 @@ def test_shard_bounds_properties():
     c = [shard_bounds(0, 10**9, 4, r, "prefix") for r in range(4)]
     widths = [b - a for a, b in c]
     assert widths == sorted(widths, reverse=True)
+
+
+def test_auto_balance_equalises_model_cost():
+    """balance="auto" (the distributed default): on the C5 prefix (0, 1e11] each
+    of 8 shards carries 1/8 of the modelled AUTO-path device time (HALF below
+    the 4e9 crossover, BSGS above), to within the 8-aligned rounding."""
+    from paper_2507_06579_b200.dist import auto_cost_density
+    X, G = 10**11, 8
+    cuts = [shard_bounds(0, X, G, r, "auto") for r in range(G)]
+    xs = np.linspace(1.0, X, 200001)
+    c = auto_cost_density(xs)
+    cum = np.concatenate([[0.0], np.cumsum(0.5 * (c[1:] + c[:-1]) * np.diff(xs))])
+    share = [np.interp(b, xs, cum) - np.interp(a, xs, cum) for a, b in cuts]
+    share = np.array(share) / cum[-1]
+    assert np.all(np.abs(share - 1 / G) < 2e-3), share
+    # the flat split would give the last shard ~1.3x the first's cost
+    assert cuts[0][1] - cuts[0][0] > cuts[-1][1] - cuts[-1][0]
