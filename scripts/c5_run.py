@@ -52,6 +52,20 @@ I = np.concatenate([[0.0], np.cumsum(0.5 * (fgrid[1:] + fgrid[:-1]) * np.diff(gr
 Ix = np.interp(xs, grid, I)
 rp = R["EP"].astype(np.float64)[m] - R["DP"].astype(np.float64)[m] / 3.0
 a_fit = float((Ix[m] @ rp) / (Ix[m] @ Ix[m]))
+# eq. (3): P(d in E | d in D) ~ 1/3 - b d^(-1/6), b ~ 0.201, fitted
+# from the E/D frequencies of consecutive windows of width 1e9 (weights = D counts)
+wb, wx, wy = [], [], []
+for lo_w in range(10**9, top, 10**9):
+    hi_w = lo_w + 10**9
+    if hi_w > top:
+        break
+    Dw = at("D", hi_w) - at("D", lo_w)
+    Ew = at("E", hi_w) - at("E", lo_w)
+    wb.append(Dw)
+    wx.append(((lo_w + hi_w) / 2) ** (-1 / 6))
+    wy.append(1 / 3 - Ew / Dw)
+wb, wx, wy = (np.asarray(v, dtype=np.float64) for v in (wb, wx, wy))
+b3 = float((wb * wx) @ wy / ((wb * wx) @ wx)) if len(wb) else float("nan")
 T2 = R["D"].astype(np.int64) - R["E"].astype(np.int64) - R["T1"].astype(np.int64)
 print(json.dumps({
     "top": top, "checkpoints": len(x), "wall_s": round(wall, 2),
@@ -63,6 +77,7 @@ print(json.dumps({
     "table1": table1, "moebius_pi_D": moeb,
     "eq1_fit_c": c, "eq1_paper_c": -0.024,
     "pdata_fit_a": a_fit, "pdata_paper_a": -0.037,
+    "eq3_fit_b": b3, "eq3_paper_b": 0.201, "eq3_windows": len(wb),
     "share_E_in_D_at_top": at("E", top) / at("D", top),
     "share_EP_in_DP_at_top": at("EP", top) / max(1, at("DP", top)),
 }, indent=1))
