@@ -136,6 +136,28 @@ def test_bsgs_options_do_not_change_results(opts):
         eis.set_option("mode", eis.MODE_AUTO)
 
 
+@pytest.mark.parametrize("hi", [10**10, 5 * 10**10, eis.MAX_D])
+def test_half_and_bsgs_agree_on_large_windows(hi):
+    """Where the oracle is too slow for every d: the half walk (no giant steps)
+    and BSGS (two-sided window, giant steps, store) are independent algorithms
+    for the same t; their flags over ~2.5e5 candidates near hi must be
+    byte-identical, and a seeded sample is checked against the oracle."""
+    lo = hi - 2 * 10**6
+    try:
+        eis.set_option("mode", eis.MODE_HALF)
+        fh = eis.classify_range(lo, hi)
+        eis.set_option("mode", eis.MODE_BSGS)
+        fb = eis.classify_range(lo, hi)
+    finally:
+        eis.set_option("mode", eis.MODE_AUTO)
+    assert np.array_equal(fh, fb)
+    first = lo + (5 - lo) % 8
+    rng = np.random.default_rng(hi % 1009)
+    pick = rng.choice(np.flatnonzero(fh != eis.NOT_IN_D), 40, replace=False)
+    want = c_oracle.classify_list((first + 8 * pick).astype(np.uint64))
+    assert np.array_equal(fh[pick], want)
+
+
 def test_auto_range_spanning_the_crossover():
     """AUTO splits a range at the crossover (HALF below, BSGS at and above it):
     flags and checkpoint counts across the split equal the oracle's."""
