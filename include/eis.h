@@ -92,7 +92,8 @@ EIS_API const char *eis_last_error(void);
 /* Tunables; unknown key or bad value -> EIS_EINVAL.  None changes a result.
  *  "mode"          EIS_MODE_* (default AUTO)
  *  "crossover"     AUTO: HALF for segments starting below this d, else BSGS
- *  "alpha_x16"     BSGS baby window W = (alpha_x16/16) d^(1/4), in [4, 64]
+ *  "alpha_x16"     BSGS baby window W = (alpha_x16/16) d^(1/4), in [4, 64]; 0 (default) =
+ *                  chosen per segment from d (measured optimum)
  *  "segment_log2"  candidates per segment (HALF; BSGS caps it by store memory)
  *  "blocks_per_sm" HALF walk kernel CTAs per SM
  *  "giant_ctas"    BSGS giant kernel CTAs per SM (0 = occupancy maximum)

@@ -58,8 +58,7 @@ struct Ctx {
     u64 crossover = 4000000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
                                      // HALF 1.08x faster at 3e9, BSGS 1.09x at 5e9, 1.27x
                                      // at 1e10, 2.2x at 1e11)
-    int alpha_x16 = 28;              // BSGS baby window W = alpha * d^(1/4) (best at 1e10,
-                                     // within 1% of the best at 1e11)
+    int alpha_x16 = 0;               // BSGS baby window W = alpha d^(1/4); 0 = by d (alpha_for)
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
     int threads = 256;
@@ -201,6 +200,20 @@ bool cand_range(u64 lo, u64 hi, u64 &i_first, u64 &i_last) {
     return true;
 }
 
+// BSGS window factor (x16) for a segment ending at d: the option, or (0) the
+// measured optimum log-interpolated over d (2.25 at 5e9, 1.75 at
+// 1e10, 1.5 at 1e11); results never depend on it (R6, R29)
+int alpha_for(u64 d) {
+    if (g.alpha_x16 > 0) return g.alpha_x16;
+    const double x = std::log10((double)d);
+    double a;
+    if (x <= 9.7) a = 36;                                  // 2.25
+    else if (x <= 10.0) a = 36 + (28 - 36) * (x - 9.7) / 0.3;
+    else if (x <= 11.0) a = 28 + (24 - 28) * (x - 10.0);
+    else a = 24;
+    return (int)std::lround(a);
+}
+
 bool want_bsgs(u64 d_lo) {
     if (g.mode == EIS_MODE_HALF) return false;
     if (g.mode == EIS_MODE_BSGS) return true;
@@ -229,7 +242,8 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     const bool bsgs = want_bsgs(cand_d(i_first));
     u64 seg_cap = SEG;
     if (bsgs) {
-        const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), g.alpha_x16 / 16.0f, g.two_sided);
+        const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), alpha_for(cand_d(i_last)) / 16.0f,
+                                                g.two_sided);
         seg_cap = std::min<u64>(SEG, std::max<u64>(((u64)g.bsgs_gb << 30) / per, 1ull << 16));
     }
     // equal segments: a short remainder segment would be all giant-kernel tail
@@ -304,11 +318,11 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
             BsgsPlan pl;
             // scratch is (re)allocated only when it must grow: drain both streams then
             // (otherwise the giant kernel of the previous segment keeps running on aux)
-            if (bsgs_needs_grow(bf.bsgs, len, d_last, g.alpha_x16, g.two_sided)) {
+            if (bsgs_needs_grow(bf.bsgs, len, d_last, alpha_for(d_last), g.two_sided)) {
                 CUDA_TRY(cudaStreamSynchronize(g.aux));
                 CUDA_TRY(cudaStreamSynchronize(s));
             }
-            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, g.alpha_x16, g.giant_ctas, g.two_sided, bf.bsgs,
+            int rc = bsgs_prepare(pl, len, d_last, g.num_sms, alpha_for(d_last), g.giant_ctas, g.two_sided, bf.bsgs,
                                   bf.ctr + 2, g.window_ctas, hist_words(a));
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
@@ -531,7 +545,8 @@ int eis_set_option(const char *key, int64_t v) {
         if (v < 0) return fail(EIS_EINVAL, "crossover must be >= 0");
         g.crossover = (u64)v;
     } else if (k == "alpha_x16") {
-        if (v < 4 || v > 64) return fail(EIS_EINVAL, "alpha_x16 must be in [4, 64]");
+        if (v != 0 && (v < 4 || v > 64))
+            return fail(EIS_EINVAL, "alpha_x16 must be 0 (by d) or in [4, 64]");
         g.alpha_x16 = (int)v;
     } else if (k == "segment_log2") {
         if (v < 18 || v > 31) return fail(EIS_EINVAL, "segment_log2 must be in [18, 31]");

@@ -78,9 +78,14 @@ def test_validation_before_device_work(lib):
         eis.set_option("no_such_option", 1)
     with pytest.raises(eis.EisError):
         eis.set_option("mode", 7)
+    assert eis.get_option("alpha_x16") == 0            # default: chosen per segment from d
     eis.set_option("alpha_x16", 32)
     assert eis.get_option("alpha_x16") == 32
-    eis.set_option("alpha_x16", 16)
+    with pytest.raises(eis.EisError):
+        eis.set_option("alpha_x16", 3)
+    eis.set_option("alpha_x16", 0)
+    for k in ("two_sided", "bsgs_gb", "window_ctas", "giant_ctas", "crossover"):
+        eis.set_option(k, eis.get_option(k))          # every documented option round-trips
     # empty inputs are no-ops
     assert eis.classify_range(6, 12).size == 0
     d, e_ = eis.count([])
