@@ -43,6 +43,12 @@ OPS_PER_BABY = 14
 GENERIC_PER_BABY = 34
 OPS_PER_GIANT = 700    # thread-instructions of one fast-path giant step (K3 BSGS)
 OPS_PER_ENTRY = 12     # store insert per window entry: slot pack, hash, bucket insert
+# DRAM bytes per d of the BSGS walk at the bench configuration: dram__bytes_read +
+# dram__bytes_write of bsgs_window + bsgs_prep + bsgs_giant for one segment (ncu
+# --set full, profiles/r01_bsgs_walk.txt: 26.38 + 0.96 + 8.36 GB) / the segment's
+# 4.22 M d.  Algorithmic: list write + read-back 3.6 KB, table 2.9 KB, ~18.5 probes
+# x 64 B, records ~0.2 KB = ~7.9 KB per d.
+BSGS_DRAM_BYTES_PER_D = 8460
 
 
 def _env_int(k, d):
@@ -340,9 +346,12 @@ def main():
             "roofline": {
                 "bound": "alu", "kernel": dom_name,
                 "achieved": achieved, "peak": peak, "unit": "Tops/s", "frac": achieved / peak,
-                "traffic": None if bsgs else 50.8e6,
-                "traffic_note": ("see profiles/ (ncu --set full of the BSGS kernels); the path "
-                                 "is issue-bound, DRAM < 40% of peak") if bsgs else
+                "traffic": BSGS_DRAM_BYTES_PER_D * nD_rank if bsgs else 50.8e6,
+                "traffic_note": ("dram read+write bytes per step of the BSGS walk: 8.46 KB per d "
+                                 "measured by ncu --set full on the bench workload "
+                                 "(profiles/r01_bsgs_walk.txt) x d per step; algorithmic ~7.9 KB "
+                                 "per d (list 3.6, table 2.9, probes 1.2, records 0.2); the "
+                                 "walk is issue/latency-bound at ~2.8 TB/s average") if bsgs else
                                 "dram read+write bytes per walk launch, ncu --set full "
                                 "(profiles/r01_half_walk.txt); algorithmic bytes = 4 per d "
                                 "(survivor list) = 50.7 MB",
