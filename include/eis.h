@@ -99,6 +99,9 @@ EIS_API const char *eis_last_error(void);
  *  "giant_ctas"    BSGS giant kernel CTAs per SM (0 = occupancy maximum)
  *  "window_ctas"   BSGS window kernel CTAs per SM (0 = occupancy maximum)
  *  "bsgs_gb"       BSGS store memory per segment buffer in GiB (two buffers), [1, 64]
+ *  "giant_cap"     BSGS giant steps per d before the exact half walk takes over:
+ *                  giant_cap * (d^(1/4) + 10), in [0, 1000] (default 20; 0 sends
+ *                  every d past k = 2 to the half walk, a test of that path)
  *  "half_ksteps"   HALF walk: rho steps per lane between refills (0 = auto, 18/36/72/144)
  *  "two_sided"     BSGS: 1 (default) = the store is also matched against conjugates and
  *                  the giant stride is mu_1^2 (R35); 0 = the paper's one-sided

@@ -64,6 +64,8 @@ struct Ctx {
     int threads = 256;
     int giant_ctas = 0;
     int window_ctas = 0;             // BSGS window kernel CTAs per SM (0 = occupancy maximum)
+    int giant_cap = 20;              // BSGS giant steps per d before the exact half walk takes
+                                     // over: giant_cap * (d^(1/4) + 10) (tests force it to 0)
     int bsgs_gb = 32;                // BSGS store memory per segment buffer (two buffers; 12 -> 32:
                                      // 293 -> ~307 M d/s, fewer giant-kernel tails)
     int half_ksteps = 0;             // 0: chosen per segment from d
@@ -323,7 +325,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
                 CUDA_TRY(cudaStreamSynchronize(s));
             }
             int rc = bsgs_prepare(pl, len, d_last, g.num_sms, alpha_for(d_last), g.giant_ctas, g.two_sided, bf.bsgs,
-                                  bf.ctr + 2, g.window_ctas, hist_words(a));
+                                  bf.ctr + 2, g.window_ctas, hist_words(a), g.giant_cap);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -528,6 +530,7 @@ void eis_finalize(void) {
     fresh.giant_ctas = g.giant_ctas;
     fresh.window_ctas = g.window_ctas;
     fresh.bsgs_gb = g.bsgs_gb;
+    fresh.giant_cap = g.giant_cap;
     fresh.half_ksteps = g.half_ksteps;
     fresh.two_sided = g.two_sided;
     g = fresh;
@@ -551,6 +554,9 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "segment_log2") {
         if (v < 18 || v > 31) return fail(EIS_EINVAL, "segment_log2 must be in [18, 31]");
         g.segment_log2 = (int)v;
+    } else if (k == "giant_cap") {
+        if (v < 0 || v > 1000) return fail(EIS_EINVAL, "giant_cap must be in [0, 1000]");
+        g.giant_cap = (int)v;
     } else if (k == "bsgs_gb") {
         if (v < 1 || v > 64) return fail(EIS_EINVAL, "bsgs_gb must be in [1, 64]");
         g.bsgs_gb = (int)v;
@@ -587,6 +593,7 @@ int64_t eis_get_option(const char *key) {
     if (k == "giant_ctas") return g.giant_ctas;
     if (k == "window_ctas") return g.window_ctas;
     if (k == "bsgs_gb") return g.bsgs_gb;
+    if (k == "giant_cap") return g.giant_cap;
     if (k == "half_ksteps") return g.half_ksteps;
     if (k == "two_sided") return g.two_sided;
     return fail(EIS_EINVAL, "unknown option '%s'", key);

@@ -1027,7 +1027,7 @@ inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
 // the launch shapes.  ctr: 4 device counters (zeroed by bsgs_launch_window).
 inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
                         int giant_ctas, int two_sided, BsgsScratch &scr, u32 *ctr,
-                        int window_ctas, u32 hist_w) {
+                        int window_ctas, u32 hist_w, int giant_cap = 20) {
     BsgsArgs &B = pl.B;
     const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided);
     B.nw = z.nw;
@@ -1035,7 +1035,7 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     B.nb = z.nb;
     B.lcap = z.lcap;
     B.plain_th = 50;
-    B.giant_cap_mul = 20.0f;
+    B.giant_cap_mul = (float)giant_cap;
     B.two_sided = two_sided;
     const size_t n = (size_t)seg_len;
     if (bsgs_grow(scr.lists, scr.lists_n, n * (size_t)z.lcap)) return -3;

@@ -84,7 +84,7 @@ def test_validation_before_device_work(lib):
     with pytest.raises(eis.EisError):
         eis.set_option("alpha_x16", 3)
     eis.set_option("alpha_x16", 0)
-    for k in ("two_sided", "bsgs_gb", "window_ctas", "giant_ctas", "crossover"):
+    for k in ("two_sided", "bsgs_gb", "window_ctas", "giant_ctas", "crossover", "giant_cap"):
         eis.set_option(k, eis.get_option(k))          # every documented option round-trips
     # empty inputs are no-ops
     assert eis.classify_range(6, 12).size == 0

@@ -119,7 +119,8 @@ def test_count_matches_oracle_and_flags(mode):
 
 
 @pytest.mark.parametrize("opts", [{"two_sided": 0}, {"bsgs_gb": 1}, {"alpha_x16": 8},
-                                  {"alpha_x16": 64, "two_sided": 0}])
+                                  {"alpha_x16": 64, "two_sided": 0}, {"giant_cap": 0},
+                                  {"giant_cap": 0, "two_sided": 0}])
 def test_bsgs_options_do_not_change_results(opts):
     """BSGS with the paper's one-sided Alg. 1 (two_sided=0), tiny store memory
     (many segments), and extreme windows: flags equal the oracle's (R6, R29, R35)."""
