@@ -736,7 +736,10 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 // lockstep.  One-sided: the lookup of mu'_2 is left to the giant kernel's
 // pipelined probe.  Two-sided (R35): mu'_2 is the stride and mu''_1; it is
 // looked up here and mu''_2 = mu''_1^2 (NUDUPL again) taken in lockstep too.
-__global__ void __launch_bounds__(256)
+#ifndef PREP_MINB
+#define PREP_MINB 4                           // measured: 2 / 3 / 4 CTAs per SM: 340 / 342 / 343 M d/s
+#endif
+__global__ void __launch_bounds__(256, PREP_MINB)
 bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     extern __shared__ u32 hist[];                       // hist_words(a)
     hist_zero(a, hist);
