@@ -811,7 +811,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #define GIANT_THREADS 128
 #endif
 #ifndef GIANT_MINB
-#define GIANT_MINB 5
+#define GIANT_MINB 6                          // 80 registers: 5 / 6 CTAs per SM measured 345 / 353 M d/s
 #endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
@@ -834,7 +834,8 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     bool exhausted = false;
     u32 head = 0, tail = 0;                            // warp-uniform ring positions
     bool qdone = false;                                // the queue is drained
-    u64 baby = 0, giant = 0, red = 0, done = 0, fb = 0;
+    u64 baby = 0;                                      // (half-walk fallback steps)
+    u32 giant = 0, red = 0, done = 0, fb = 0;          // per-thread counts fit in 32 bits
     u32 err = 0;
 
     for (;;) {
