@@ -668,7 +668,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     __syncthreads();
     const u32 n = *a.count;
     const int nblk = B.nw / 8;
-    u64 baby = 0, done = 0, sym = 0;
+    u32 baby = 0, done = 0, sym = 0;                    // per-thread counts fit in 32 bits
     for (;;) {
         u32 wave = 0;
         if (lane == 0) wave = atomicAdd(a.work, 1u);
