@@ -811,7 +811,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #define GIANT_THREADS 128
 #endif
 #ifndef GIANT_MINB
-#define GIANT_MINB 6                          // 80 registers: 5 / 6 CTAs per SM measured 345 / 353 M d/s
+#define GIANT_MINB 7                          // 72 registers: 5 / 6 / 7 CTAs per SM measured 345 / 354 / 358 M d/s
 #endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
@@ -827,7 +827,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 nq = o.ctr[2];
-    const u32 *tab = nullptr, *list = nullptr;
+    u32 gidx = 0;                                      // the lane's survivor (store index)
     GiantLane g;
     g.phase = PH_IDLE;
     u32 off = 0;
@@ -868,8 +868,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                     const GiantRec rec = stash[wid][sl];
                     off = rec.off;                        // (with the prime bit)
                     giant_unpack(g, rec, cand_d(a.i0 + (off & ~PRIME_BIT)));
-                    tab = o.tables + (u64)idx * ((u64)B.nb * BKT);
-                    list = o.lists + (u64)idx * B.lcap;
+                    gidx = idx;
                 } else {
                     exhausted = true;                     // (only when qdone)
                 }
@@ -880,6 +879,9 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         if (__all_sync(FULL_MASK, exhausted && g.phase == PH_IDLE)) break;
         const u32 gmask = __ballot_sync(FULL_MASK, g.phase == PH_GIANT);
         if (g.phase == PH_GIANT) {
+            // (pointers recomputed from the 32-bit index: fewer live registers)
+            const u32 *tab = o.tables + (u64)gidx * ((u64)B.nb * BKT);
+            const u32 *list = o.lists + (u64)gidx * B.lcap;
             // software pipeline: probe mu'_k (refills start with mu'_2, not yet
             // probed) while computing mu'_{k+1}
             // probed while computing mu'_{k+1}; the bucket is copied to shared
