@@ -323,13 +323,14 @@ EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
 // The fixed left operand of every giant step (mu_1), normalised as in Alg. 4
 // (P mod Q, w = (P^2 - d)/(2Q)) once per d.
 struct Mu1Form {
-    i64 Q, P, w;
+    u32 Q, P;           // < 2^20 (reduced); 32-bit to keep the giant lane state small
+    i64 w;
 };
 EIS_HD Mu1Form mu1_form(i64 Q1, i64 P1, i64 d, u32 *err) {
     Mu1Form f;
     f.Q = Q1;
     f.P = floor_mod(P1, Q1);
-    f.w = exact_div(f.P * f.P - d, 2 * Q1, err);
+    f.w = exact_div((i64)f.P * f.P - d, 2 * Q1, err);
     return f;
 }
 

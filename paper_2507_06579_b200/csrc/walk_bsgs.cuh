@@ -322,8 +322,8 @@ EIS_HD BabyRec win_pack(const WinLane &w, u32 off, u32 n) {
 // ----------------------------------------------------------- giant phase --
 struct GiantLane {
     u64 d;
-    i64 s, L;           // isqrt(d), floor(d^(1/4))
-    double sqrtd;
+    u32 s, L;           // isqrt(d) < 2^19, floor(d^(1/4)) (32-bit: fewer live registers)
+    float sqrtd;        // only feeds fp32 log2 distances and NUCOMP's float bound
     Mu1Form m1;
     u32 t1;
     float dist1, dist_last;
@@ -335,9 +335,9 @@ struct GiantLane {
 
 EIS_HD void giant_init(GiantLane &g, const BsgsArgs &B, u64 d, const BabyRec &br, u32 *err) {
     g.d = d;
-    g.s = (i64)isqrt_u64_dev(d);
-    g.L = (i64)isqrt_u64_dev((u64)g.s);            // floor(d^(1/4))
-    g.sqrtd = sqrt((double)d);
+    g.s = isqrt_u64_dev(d);
+    g.L = isqrt_u64_dev((u64)g.s);                 // floor(d^(1/4))
+    g.sqrtd = (float)sqrt((double)d);
     g.m1 = mu1_form((i64)br.Q1, (i64)br.P1, (i64)d, err);
     g.t1 = br.t1;
     g.dist1 = br.dist1;
@@ -362,7 +362,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
     GiantInfo gi;
     const i64 d = (i64)g.d;
     const i64 s = g.s;
-    const GiantComp c = giant_compose(g.m1, (i64)g.Qc, (i64)g.Pc, d, s, g.L, (float)g.sqrtd,
+    const GiantComp c = giant_compose(g.m1, (i64)g.Qc, (i64)g.Pc, d, s, (i64)g.L, g.sqrtd,
                                       B.plain_th, err, wmask);
     warp_reconverge(wmask);
     gi.kind = c.kind;
@@ -385,7 +385,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
             const double Qn = rint((double)nQ * rQ);
             if ((i64)Qn * (i64)Qd != nQ) *err += 1;
             t = mod3_small(t + 1u + (u32)((Pni >> 1) & 1));
-            dist += log2_approx((float)fabs(Pn + g.sqrtd)) - log2_approx((float)Qd);
+            dist += log2_approx((float)fabs(Pn + (double)g.sqrtd)) - log2_approx((float)Qd);
             Qd = fabs(Qn);
             rQ = rcp64(Qd);
             Pd = sd - dfloor_mod(sd - Pn, Qd, rQ);   // canonical P in (s - Q, s]
@@ -489,12 +489,12 @@ EIS_HD GiantRec giant_pack(const GiantLane &g, u32 off) {
 
 EIS_HD void giant_unpack(GiantLane &g, const GiantRec &r, u64 d) {
     g.d = d;
-    g.s = (i64)r.s;
-    g.L = (i64)(r.Lk & 0xFFFFu);
+    g.s = r.s;
+    g.L = r.Lk & 0xFFFFu;
     g.kcap = (int)(r.Lk >> 16);
-    g.sqrtd = r.sqrtd;
-    g.m1.Q = (i64)r.Q1;
-    g.m1.P = (i64)r.P1;
+    g.sqrtd = (float)r.sqrtd;
+    g.m1.Q = r.Q1;
+    g.m1.P = r.P1;
     g.m1.w = r.w1;
     g.t1 = r.tk & 3u;
     g.tc = (r.tk >> 2) & 3u;
@@ -766,7 +766,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             const GiantInfo gi = giant_start(g, B, &err, kmask);
             giant++;
             red += gi.nred;
-            two = g.m1.Q == (i64)g.Qc && g.dist1 == g.distc;   // stride = mu'_2 (R35)
+            two = g.m1.Q == g.Qc && g.dist1 == g.distc;   // stride = mu'_2 (R35)
         }
         // two-sided: look up mu''_1 = mu'_2 here and take mu''_2 = mu''_1^2 (NUDUPL,
         // the generic path) in lockstep, so the giant kernel composes distinct ideals
