@@ -577,6 +577,9 @@ __device__ __forceinline__ void smem_st(u32 addr, u32 v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+#ifndef BUILD_K
+#define BUILD_K 2
+#endif
 // One store, built by the whole warp in shared memory (tab: nb * BKT slots, cnt:
 // nb fill counters, both zero on entry and on exit) and written to dst.
 __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, u32 nb, u32 *tab,
@@ -589,26 +592,27 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
     // lists are padded to lcap (a multiple of 32), so the loads stay in bounds
     const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
     const u32 n4 = (n + 3) >> 2;
-    uint4 nx[2];
+    constexpr int K = BUILD_K;                       // 16-byte loads per lane per group
+    uint4 nx[K];
 #pragma unroll
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < K; k++) {
         const u32 i4 = (u32)(32 * k + lane);
         nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
     }
-    for (u32 jb = 0; jb < n; jb += 256) {
-        uint4 cur[2];
+    for (u32 jb = 0; jb < n; jb += 128 * K) {
+        uint4 cur[K];
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
+        for (int k = 0; k < K; k++) {
             cur[k] = nx[k];
-            const u32 i4 = jb / 4 + (u32)(64 + 32 * k + lane);
+            const u32 i4 = jb / 4 + (u32)(32 * K + 32 * k + lane);
             nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
         }
-        // first attempts for the group's 8 entries per lane back to back (their
-        // atomics overlap), then one warp-uniform loop for full buckets (rare)
+        // first attempts for the group's entries, then one warp-uniform loop for
+        // full buckets (rare)
         u32 ovf = 0;                                     // bit i: entry i still to place
-        u32 bb[8], sv[8];
+        u32 bb[4 * K], sv[4 * K];
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
+        for (int k = 0; k < K; k++) {
 #pragma unroll
             for (int w = 0; w < 4; w++) {
                 const int i = 4 * k + w;
@@ -627,7 +631,7 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
         while (__any_sync(FULL_MASK, ovf)) {
             if (ovf) {
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
+                for (int i = 0; i < 4 * K; i++) {
                     if (ovf & (1u << i)) {
                         bb[i] = next_bucket(bb[i], nb);
                         const u32 pos = smem_atom_inc(cnt_s + 4 * bb[i]);
@@ -676,16 +680,13 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         if ((u64)wave * 32 >= n) break;
         const u32 idx = wave * 32 + lane;
         const bool has = idx < n;
-        u32 off = 0;
-        u64 d = 0;
         WinLane w;
         win_idle(w);
         u32 e[8];
         e[0] = e[1] = 0;
-        if (has) {
-            off = __ldg(a.list + idx);
-            d = cand_d(a.i0 + (off & ~PRIME_BIT));
-            win_begin(w, d, e[0], e[1]);
+        if (has) {   // (offset and d are re-read at the end: fewer live registers)
+            const u32 off0 = __ldg(a.list + idx);
+            win_begin(w, cand_d(a.i0 + (off0 & ~PRIME_BIT)), e[0], e[1]);
         }
         u32 *lst = o.lists + (u64)idx * B.lcap;
         if (w.live) baby += 7;                           // theta_2 (closed form) + 6
@@ -712,11 +713,12 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             }
         }
         if (has && !w.live) {                            // symmetry exit (or d < 8)
-            record_result(a, hist, off, d, w.res);
+            const u32 off = __ldg(a.list + idx);
+            record_result(a, hist, off, cand_d(a.i0 + (off & ~PRIME_BIT)), w.res);
             done++;
             sym++;
         }
-        if (w.live) o.brecs[idx] = win_pack(w, off, (u32)B.nw);
+        if (w.live) o.brecs[idx] = win_pack(w, __ldg(a.list + idx), (u32)B.nw);
         const u32 live = __ballot_sync(FULL_MASK, w.live);
         for (u32 m = live; m; m &= m - 1) {
             const u32 i = wave * 32 + (u32)(__ffs(m) - 1);
