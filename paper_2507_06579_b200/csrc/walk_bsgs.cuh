@@ -582,30 +582,41 @@ __device__ __forceinline__ void smem_st(u32 addr, u32 v) {
 #endif
 // One store, built by the whole warp in shared memory (tab: nb * BKT slots, cnt:
 // nb fill counters, both zero on entry and on exit) and written to dst.
-__device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, u32 nb, u32 *tab,
-                                            u32 *cnt, u32 *__restrict__ dst) {
+__device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[BUILD_K]) {
+    const int lane = threadIdx.x & 31;
+    const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
+    const u32 n4 = (n + 3) >> 2;
+#pragma unroll
+    for (int k = 0; k < BUILD_K; k++) {
+        const u32 i4 = (u32)(32 * k + lane);
+        nx[k] = (lst && i4 < n4) ? l4[i4] : make_uint4(0, 0, 0, 0);
+    }
+}
+
+// nx: this d's first list group on entry (the caller or the previous call loaded
+// it); the next d's (lst_next) on exit, so list read-back latency overlaps the
+// previous d's inserts.
+__device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u32 *lst_next,
+                                            u32 n, u32 nb, u32 *tab, u32 *cnt,
+                                            u32 *__restrict__ dst, uint4 (&nx)[BUILD_K]) {
     const int lane = threadIdx.x & 31;
     const u32 tab_s = (u32)__cvta_generic_to_shared(tab);   // shared-window addresses
     const u32 cnt_s = (u32)__cvta_generic_to_shared(cnt);
-    // the lists come back from DRAM (far more of them are in flight than L2
-    // holds): 16-byte loads run one group of 256 entries (2 per lane) ahead;
-    // lists are padded to lcap (a multiple of 32), so the loads stay in bounds
     const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
     const u32 n4 = (n + 3) >> 2;
     constexpr int K = BUILD_K;                       // 16-byte loads per lane per group
-    uint4 nx[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        const u32 i4 = (u32)(32 * k + lane);
-        nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
-    }
     for (u32 jb = 0; jb < n; jb += 128 * K) {
         uint4 cur[K];
 #pragma unroll
-        for (int k = 0; k < K; k++) {
-            cur[k] = nx[k];
-            const u32 i4 = jb / 4 + (u32)(32 * K + 32 * k + lane);
-            nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
+        for (int k = 0; k < K; k++) cur[k] = nx[k];
+        if (jb + 128 * K < n) {
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                const u32 i4 = jb / 4 + (u32)(32 * K + 32 * k + lane);
+                nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
+            }
+        } else {
+            load_group0(lst_next, n, nx);            // the next d's first group
         }
         // first attempts for the group's entries, then one warp-uniform loop for
         // full buckets (rare)
@@ -628,6 +639,7 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, u32 n, 
                 }
             }
         }
+
         while (__any_sync(FULL_MASK, ovf)) {
             if (ovf) {
 #pragma unroll
@@ -720,10 +732,16 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         if (w.live) o.brecs[idx] = win_pack(w, __ldg(a.list + idx), (u32)B.nw);
         const u32 live = __ballot_sync(FULL_MASK, w.live);
+        uint4 nx[BUILD_K];
+        if (live)
+            load_group0(o.lists + (u64)(wave * 32 + (u32)(__ffs(live) - 1)) * B.lcap, (u32)B.nw, nx);
         for (u32 m = live; m; m &= m - 1) {
             const u32 i = wave * 32 + (u32)(__ffs(m) - 1);
-            build_store(o.lists + (u64)i * B.lcap, (u32)B.nw, nb, tab, cnt,
-                        o.tables + (u64)i * ((u64)nb * BKT));
+            const u32 m2 = m & (m - 1);
+            const u32 *next = m2 ? o.lists + (u64)(wave * 32 + (u32)(__ffs(m2) - 1)) * B.lcap
+                                 : nullptr;
+            build_store(o.lists + (u64)i * B.lcap, next, (u32)B.nw, nb, tab, cnt,
+                        o.tables + (u64)i * ((u64)nb * BKT), nx);
         }
         u32 qb = 0;
         if (lane == 0 && live) qb = atomicAdd(&o.ctr[0], (u32)__popc(live));
