@@ -656,13 +656,20 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
             }
         }
     }
+    // write out with one TMA bulk copy (shared -> global, one lane; cp.async.bulk),
+    // then clear the table once the copy has read it.  Per-lane 16-byte copies
+    // through registers measured 2.5% slower on the bench line.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-    uint4 *s4 = reinterpret_cast<uint4 *>(tab);
-    for (u32 i = lane; i < nb * (BKT / 4); i += 32) {  // write out, clear for the next d
-        d4[i] = s4[i];
-        s4[i] = make_uint4(0, 0, 0, 0);
+    if (lane == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(dst), "r"(tab_s), "r"(nb * BKT * 4u) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
+    __syncwarp();
+    uint4 *s4 = reinterpret_cast<uint4 *>(tab);
+    for (u32 i = lane; i < nb * (BKT / 4); i += 32) s4[i] = make_uint4(0, 0, 0, 0);
     for (u32 i = lane; i < nb; i += 32) cnt[i] = 0;
     __syncwarp();
 }
