@@ -104,11 +104,17 @@ EIS_HD float ffloor_div_pos(float a, float b) {   // floor(a/b), 0 <= a, 0 < b, 
     return q;
 }
 
-// g = gcd(a, b) and x with x a = g (mod b), for 0 <= a, b < 2^24 (exact floats).
+// g = gcd(a, b) and x with x a = g (mod b), for 0 <= a, b < 2^20 (exact floats).
+// Nearest-integer Euclid with signed remainders: q = round(a * rcp(b)) is
+// within 1/2 + 1/4 of a/b (|a/b| < 2^20, relative rcp error < 2^-22), so
+// |r| <= 3/4 |b| and no correction step is needed.  About 30% fewer iterations than the
+// floor-quotient loop (R36).  x is correct modulo b/g, which is all
+// NUCOMP uses (Alg. 2 l.626-634: b enters only through b u2 = F (mod u1)).
+constexpr float RMAGIC = 12582912.0f;  // 1.5 * 2^23: round to nearest for |v| < 2^22
 EIS_HD float fxgcd_x(float a, float b, float &x) {
     float x0 = 1.f, x1 = 0.f;
     while (b != 0.f) {
-        const float q = ffloor_div_pos(a, b);
+        const float q = fmaf(a, rcp_approx(b), RMAGIC) - RMAGIC;
         const float r = fmaf(-q, b, a);
         a = b;
         b = r;
@@ -116,8 +122,8 @@ EIS_HD float fxgcd_x(float a, float b, float &x) {
         x0 = x1;
         x1 = t;
     }
-    x = x0;
-    return a;
+    x = a < 0.f ? -x0 : x0;
+    return fabsf(a);
 }
 
 // exact division of small integers: |a| < 2^23, 0 < b < 2^23, b | a

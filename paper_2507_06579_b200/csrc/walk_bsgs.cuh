@@ -167,21 +167,30 @@ EIS_HD u32 bucket_slot(const Probe &p, int i) {      // i: compile-time after un
     return k == 0 ? g.x : (k == 1 ? g.y : (k == 2 ? g.z : g.w));
 }
 
+// Slots before the first empty one (all 16 if the bucket is full).
+EIS_HD_COLD u32 filled_mask(const Probe &p) {
+    u32 em = 0;
+#pragma unroll
+    for (int i = 0; i < BKT; i++) em |= (u32)(bucket_slot(p, i) == 0) << i;
+    return (em & (0u - em)) - 1u;
+}
+
 // Resolve a probe of (Q, P): the hit kind, t3 = t(theta) mod 3, j = the entry.
-// The bucket is scanned without branches (key-match and empty-slot masks); a
+// The bucket is scanned without branches: bit i of the key-match mask is bit 31
+// of ((slot_i ^ qk) & 0x3FFFF) - 1.  A bucket fills in slot order (one counter
+// per bucket in the build), so it is full iff its last slot is, and an empty slot
+// (0) can match only key 0 (Q = 2), which masks the empty slots off (rare).  A
 // key match (about one per d) re-reads its slot and checks P (R34, R35).
 EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d, u32 s,
                          u32 Q, u32 P, u32 &t3, u32 &j) {
     const u32 qk = Q >> 2;
     for (;;) {
-        u32 mm = 0, em = 0;
+        u32 mm = 0;
 #pragma unroll
-        for (int i = 0; i < BKT; i++) {
-            const u32 e = bucket_slot(p, i);
-            mm |= (u32)((e & 0x3FFFFu) == qk) << i;
-            em |= (u32)(e == 0) << i;
-        }
-        mm &= (em & (0u - em)) - 1u;                   // slots before the first empty one
+        for (int i = BKT - 1; i >= 0; i--)
+            mm = (mm << 1) | ((((bucket_slot(p, i) ^ qk) & 0x3FFFFu) - 1u) >> 31);
+        const bool full = bucket_slot(p, BKT - 1) != 0;
+        if (qk == 0) mm &= filled_mask(p);
         while (mm) {
             const int i = __builtin_ctz_portable(mm);
             mm &= mm - 1;
@@ -195,7 +204,7 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
                 return k;
             }
         }
-        if (em) return HIT_NONE;
+        if (!full) return HIT_NONE;
         load_bucket(tab, next_bucket(p.b, nb), p);       // bucket full: continue
     }
 }
