@@ -147,6 +147,7 @@ struct WalkArgs {
     int b_lo, nb;        // bucket range of this segment: [b_lo, b_lo+nb)
     int n_ckpt;
     int nrow;            // count rows (2 or NROW_MAX)
+    u32 hist_w;          // hist_words_of(ckpt, nrow, nb), set on the host
     u64 *buckets;        // device: [nrow][n_ckpt] counts (row order above)
     u64 *stats;          // device: EisStatSlot counters
     u32 *err;            // device: invariant-violation counter
@@ -168,9 +169,12 @@ __device__ __forceinline__ int bucket_of(const u64 *x, int lo, int hi, u64 d) {
 
 // shared-memory words of a walk kernel's histogram (dynamic shared memory, a
 // multiple of 4 so that what follows stays 16-byte aligned)
-inline __host__ __device__ u32 hist_words(const WalkArgs &a) {
-    return a.ckpt ? ((u32)(a.nrow * a.nb) + 3u) & ~3u : 0u;
+inline __host__ __device__ u32 hist_words_of(const void *ckpt, int nrow, int nb) {
+    return ckpt ? ((u32)(nrow * nb) + 3u) & ~3u : 0u;
 }
+// (a precomputed field: the compiler rematerialises it inside hot loops, where
+// a single constant load is much cheaper than the expression)
+inline __host__ __device__ u32 hist_words(const WalkArgs &a) { return a.hist_w; }
 
 #ifdef __CUDACC__
 __device__ __forceinline__ void hist_zero(const WalkArgs &a, u32 *hist) {

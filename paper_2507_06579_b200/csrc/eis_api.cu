@@ -314,6 +314,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.nb = nb;
         a.n_ckpt = n;
         a.nrow = nrow;
+        a.hist_w = hist_words_of(a.ckpt, nrow, nb);
         a.buckets = buckets_dev;
         a.stats = g.d_stats;
         if (bsgs) {

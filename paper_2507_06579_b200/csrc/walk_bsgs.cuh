@@ -585,6 +585,9 @@ __device__ __forceinline__ u32 smem_atom_inc(u32 addr) {
 __device__ __forceinline__ void smem_st(u32 addr, u32 v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void smem_st4_zero(u32 addr) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
+}
 
 #ifndef BUILD_K
 #define BUILD_K 2
@@ -605,12 +608,11 @@ __device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[B
 // nx: this d's first list group on entry (the caller or the previous call loaded
 // it); the next d's (lst_next) on exit, so list read-back latency overlaps the
 // previous d's inserts.
+// tab_s, cnt_s: shared-window addresses of the warp's table and counters.
 __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u32 *lst_next,
-                                            u32 n, u32 nb, u32 *tab, u32 *cnt,
+                                            u32 n, u32 nb, u32 tab_s, u32 cnt_s,
                                             u32 *__restrict__ dst, uint4 (&nx)[BUILD_K]) {
     const int lane = threadIdx.x & 31;
-    const u32 tab_s = (u32)__cvta_generic_to_shared(tab);   // shared-window addresses
-    const u32 cnt_s = (u32)__cvta_generic_to_shared(cnt);
     const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
     const u32 n4 = (n + 3) >> 2;
     constexpr int K = BUILD_K;                       // 16-byte loads per lane per group
@@ -677,9 +679,8 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     __syncwarp();
-    uint4 *s4 = reinterpret_cast<uint4 *>(tab);
-    for (u32 i = lane; i < nb * (BKT / 4); i += 32) s4[i] = make_uint4(0, 0, 0, 0);
-    for (u32 i = lane; i < nb; i += 32) cnt[i] = 0;
+    for (u32 i = lane; i < nb * (BKT / 4); i += 32) smem_st4_zero(tab_s + 16 * i);
+    for (u32 i = lane; i < nb; i += 32) smem_st(cnt_s + 4 * i, 0u);
     __syncwarp();
 }
 
@@ -693,10 +694,10 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 nb = (u32)B.nb;
     const u32 wstride = window_smem_words(nb);               // 16-byte aligned per warp
-    u32 *tab = smem + hist_words(a) + (size_t)wid * wstride;
-    u32 *cnt = tab + nb * BKT;
+    const u32 tab_s = (u32)__cvta_generic_to_shared(smem) + 4u * (hist_words(a) + wid * wstride);
+    const u32 cnt_s = tab_s + 4u * nb * BKT;
     hist_zero(a, hist);
-    for (u32 i = lane; i < wstride; i += 32) tab[i] = 0;
+    for (u32 i = lane; i < wstride; i += 32) smem_st(tab_s + 4 * i, 0u);
     __syncthreads();
     const u32 n = *a.count;
     const int nblk = B.nw / 8;
@@ -756,7 +757,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             const u32 m2 = m & (m - 1);
             const u32 *next = m2 ? o.lists + (u64)(wave * 32 + (u32)(__ffs(m2) - 1)) * B.lcap
                                  : nullptr;
-            build_store(o.lists + (u64)i * B.lcap, next, (u32)B.nw, nb, tab, cnt,
+            build_store(o.lists + (u64)i * B.lcap, next, (u32)B.nw, nb, tab_s, cnt_s,
                         o.tables + (u64)i * ((u64)nb * BKT), nx);
         }
         u32 qb = 0;
