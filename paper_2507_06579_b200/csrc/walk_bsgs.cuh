@@ -694,7 +694,10 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 nb = (u32)B.nb;
     const u32 wstride = window_smem_words(nb);               // 16-byte aligned per warp
-    const u32 tab_s = (u32)__cvta_generic_to_shared(smem) + 4u * (hist_words(a) + wid * wstride);
+    // (through a shuffle: ptxas cannot rematerialise it, and otherwise rebuilt the
+    // shared-window base from SR_CgaCtaId before every table store)
+    const u32 tab_s = __shfl_sync(FULL_MASK, (u32)__cvta_generic_to_shared(smem) +
+                                                 4u * (hist_words(a) + wid * wstride), 0);
     const u32 cnt_s = tab_s + 4u * nb * BKT;
     hist_zero(a, hist);
     for (u32 i = lane; i < wstride; i += 32) smem_st(tab_s + 4 * i, 0u);
