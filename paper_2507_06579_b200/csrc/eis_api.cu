@@ -55,9 +55,9 @@ struct Ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // options
     int mode = EIS_MODE_AUTO;
-    u64 crossover = 4000000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
-                                     // HALF 1.08x faster at 3e9, BSGS 1.09x at 5e9, 1.27x
-                                     // at 1e10, 2.2x at 1e11)
+    u64 crossover = 2500000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
+                                     // HALF 1.06x faster at 2e9, BSGS 1.07x at 3e9, 1.16x
+                                     // at 4e9, 1.46x at 1e10, 2.5x at 1e11)
     int alpha_x16 = 0;               // BSGS baby window W = alpha d^(1/4); 0 = by d (alpha_for)
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
@@ -209,9 +209,9 @@ int alpha_for(u64 d) {
     if (g.alpha_x16 > 0) return g.alpha_x16;
     const double x = std::log10((double)d);
     double a;
-    if (x <= 9.7) a = 36;                                  // 2.25
-    else if (x <= 10.0) a = 36 + (28 - 36) * (x - 9.7) / 0.3;
-    else if (x <= 11.0) a = 28 + (24 - 28) * (x - 10.0);
+    if (x <= 9.7) a = 32;                                  // 2.0
+    else if (x <= 10.0) a = 32 + (28 - 32) * (x - 9.7) / 0.3;
+    else if (x <= 10.5) a = 28 + (24 - 28) * (x - 10.0) / 0.5;
     else a = 24;
     return (int)std::lround(a);
 }
@@ -253,6 +253,24 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         const u64 total = i_last - i_first + 1;
         const u64 nseg = (total + seg_cap - 1) / seg_cap;
         seg_cap = (total + nseg - 1) / nseg;
+    }
+    // BSGS scratch: reserved once per range, for a full segment at the larger of
+    // the two ends' window sizes (growing it segment by segment drained both
+    // streams and reallocated tens of GiB on most segments of a prefix run)
+    if (bsgs) {
+        const u64 d_a = cand_d(i_first), d_b = cand_d(i_last);
+        const BsgsSizes za = bsgs_sizes(d_a, alpha_for(d_a) / 16.0f, g.two_sided);
+        const BsgsSizes zb = bsgs_sizes(d_b, alpha_for(d_b) / 16.0f, g.two_sided);
+        const int lcap = std::max(za.lcap, zb.lcap), nbk = std::max(za.nb, zb.nb);
+        for (SegBuf &b : g.buf) {
+            if (b.bsgs.lists && b.bsgs.lists_n >= seg_cap * (size_t)lcap &&
+                b.bsgs.tables_n >= seg_cap * (size_t)nbk * BKT && b.bsgs.brecs_n >= seg_cap)
+                continue;
+            CUDA_TRY(cudaStreamSynchronize(g.aux));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (bsgs_reserve(b.bsgs, (size_t)seg_cap, lcap, nbk))
+                return fail(EIS_ENOMEM, "BSGS scratch allocation failed");
+        }
     }
     CUDA_TRY(cudaEventRecord(g.ev[2], s));
     int iseg = 0;

@@ -1063,6 +1063,18 @@ inline bool bsgs_needs_grow(const BsgsScratch &scr, u64 seg_len, u64 d_hi, int a
            n > scr.bqueue_n || n > scr.gqueue_n;
 }
 
+// Grow the scratch to hold a segment of n survivors with lcap list words and nb
+// buckets each (no-op when it already does).  The caller drains the streams first.
+inline int bsgs_reserve(BsgsScratch &scr, size_t n, int lcap, int nb) {
+    if (bsgs_grow(scr.lists, scr.lists_n, n * (size_t)lcap)) return -3;
+    if (bsgs_grow(scr.tables, scr.tables_n, n * (size_t)nb * BKT)) return -3;
+    if (bsgs_grow(scr.brecs, scr.brecs_n, n)) return -3;
+    if (bsgs_grow(scr.grecs, scr.grecs_n, n)) return -3;
+    if (bsgs_grow(scr.bqueue, scr.bqueue_n, n)) return -3;
+    if (bsgs_grow(scr.gqueue, scr.gqueue_n, n)) return -3;
+    return 0;
+}
+
 inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
     const BsgsSizes z = bsgs_sizes(d_max, alpha, two_sided);
     return (size_t)4 * z.lcap + (size_t)64 * z.nb + sizeof(BabyRec) + sizeof(GiantRec) + 8;
@@ -1083,13 +1095,7 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     B.plain_th = 50;
     B.giant_cap_mul = (float)giant_cap;
     B.two_sided = two_sided;
-    const size_t n = (size_t)seg_len;
-    if (bsgs_grow(scr.lists, scr.lists_n, n * (size_t)z.lcap)) return -3;
-    if (bsgs_grow(scr.tables, scr.tables_n, n * (size_t)z.nb * BKT)) return -3;
-    if (bsgs_grow(scr.brecs, scr.brecs_n, n)) return -3;
-    if (bsgs_grow(scr.grecs, scr.grecs_n, n)) return -3;
-    if (bsgs_grow(scr.bqueue, scr.bqueue_n, n)) return -3;
-    if (bsgs_grow(scr.gqueue, scr.gqueue_n, n)) return -3;
+    if (bsgs_reserve(scr, (size_t)seg_len, z.lcap, z.nb)) return -3;
     BsgsOut &o = pl.o;
     o.lists = scr.lists;
     o.tables = scr.tables;

@@ -15,4 +15,6 @@ for combo in itertools.product(*vals):
     cD, cE = eis.count_window(lo, [hi])
     st = eis.get_stats()
     print(json.dumps({**dict(zip(keys, combo)), "E": int(cE[0]), "ms": round(st["total_ms"], 2),
-                      "rate_M": round(st["d_classified"] / st["total_ms"] / 1e3, 1)}), flush=True)
+                      "rate_M": round(st["d_classified"] / st["total_ms"] / 1e3, 1),
+                      "win": round(st.get("window_ms", 0), 2), "giant": round(st.get("giant_ms", 0), 2)}),
+          flush=True)
