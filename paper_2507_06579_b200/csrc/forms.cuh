@@ -92,16 +92,18 @@ EIS_HD i64 xgcd_s(i64 a, i64 b, i64 &x, i64 &y) {
 }
 
 // ---- Euclid in exact FP32 integer arithmetic.  Every value below is an
-// integer of magnitude < 2^24, so FFMA/FADD on them are exact; the quotient
-// round(a * rcp(b)) is floor(a/b) or floor(a/b)+1 (|a/b| < 2^20, relative rcp
-// error < 2^-22) and one compare fixes it.  No integer<->float conversion
-// inside the loops (the XU pipe is narrow).
+// integer of magnitude < 2^24, so FFMA/FADD on them are exact.  No
+// integer<->float conversion inside the loops (the XU pipe is narrow).
 constexpr float FMAGIC = 8388608.0f;   // 2^23
 
-EIS_HD float ffloor_div_pos(float a, float b) {   // floor(a/b), 0 <= a, 0 < b, exact ints
-    float q = fmaf(a, rcp_approx(b), FMAGIC) - FMAGIC;
-    if (fmaf(-q, b, a) < 0.f) q -= 1.f;
-    return q;
+// floor(a/b) for integers 0 <= a < 2^20, 0 < b, with no correction step (the
+// baby step's rule, walk_bsgs.cuh baby_step_fd): rqb = rcp(b)(1 + 2^-21) lies in
+// [1/b, (1 + 2^-20)/b) (rcp error <= 2^-23), so a rqb - a/b < a 2^-20 / b < 1/b,
+// which is at most the gap between a/b and the next integer; the
+// round-toward-zero FFMA then truncates a rqb to floor(a/b).
+EIS_HD float ffloor_div_pos(float a, float b) {
+    const float rqb = rcp_approx(b) * 1.000000476837158203125f;
+    return fma_rz(a, rqb, FMAGIC) - FMAGIC;
 }
 
 // g = gcd(a, b) and x with x a = g (mod b), for 0 <= a, b < 2^20 (exact floats).
@@ -176,7 +178,7 @@ EIS_HD float log2_gamma(i64 G, i64 x, i64 y, i64 u3, i64 v3, float sqrtd_f, i64 
 }
 
 // Partial Euclid of Algs. 2-3, in exact FP32
-// (0 <= bx < by < 2^23 on entry: bx = Bx mod By, By = u1/G).
+// (0 <= bx < by < 2^19 on entry: bx = Bx mod By, By = u1/G, u1 = Q1/2 < 2^19).
 EIS_HD void partial_euclid(i64 &bx, i64 &by, i64 &x, i64 &y, int &z, i64 L) {
     float fbx = (float)bx, fby = (float)by, fx = 1.f, fy = 0.f;
     const float fL = (float)L;

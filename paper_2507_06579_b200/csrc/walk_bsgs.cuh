@@ -145,7 +145,7 @@ enum HitKind : int { HIT_NONE = 0, HIT_DIRECT = 1, HIT_CONJ = 2 };
 
 // P-bar: the canonical representative in (s - Q, s] of -P mod Q
 EIS_HD u32 conj_P(u32 Q, u32 P, u32 s) {     // = floor((s + P)/Q) Q - P (a rho step's P)
-    const float q = ffloor_div_pos((float)(s + P), (float)Q);   // exact: s + P, Q < 2^21
+    const float q = ffloor_div_pos((float)(s + P), (float)Q);   // exact: s + P < 2^20
     return (u32)q * Q - P;
 }
 
