@@ -851,7 +851,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #define GIANT_THREADS 128
 #endif
 #ifndef GIANT_MINB
-#define GIANT_MINB 7                          // 72 registers: 5 / 6 / 7 CTAs per SM measured 345 / 354 / 358 M d/s
+#define GIANT_MINB 8                          // 64 registers: 7 / 8 CTAs per SM measured 394.4 / 395.6 M d/s (earlier: 5 / 6 / 7 -> 345 / 354 / 358)
 #endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
