@@ -475,6 +475,54 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     return true;
 }
 
+// NUDUPL (Alg. 3) in the same exact fp64/FP32 arithmetic as
+// nucomp_d: the prep kernel's two doublings per d (mu_1^2, then mu''_1^2 when
+// two-sided).  Same steps and names as nudupl() above.  yy comes from the
+// nearest-integer xgcd (R36): yy v = G (mod u); Bx needs it only mod By = u/G.
+EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, u32 wmask) {
+    float fyy;
+    const float Gf = fxgcd_x(fabsf((float)v), (float)u, fyy);   // fyy |v| = G (mod u)
+    warp_reconverge(wmask);
+    const double G = (double)Gf;
+    const double rG = rcp64(G);
+    const double By = rint(u * rG), Dy = rint(v * rG);
+    const double rBy = rcp64(By);
+    const double yy = v < 0.0 ? -(double)fyy : (double)fyy;
+    const double Bx = dfloor_mod(dfloor_mod(yy, By, rBy) * dfloor_mod(w, By, rBy), By, rBy);
+    // partial Euclid (Alg. 3 l.694-700) in exact FP32, as in nucomp_d
+    float fbx = (float)Bx, fby = (float)By, fx = 1.f, fy = 0.f;
+    int z = 0;
+    while (fby > L && fbx != 0.f) {
+        const float q = ffloor_div_pos(fby, fbx);
+        const float t = fmaf(-q, fbx, fby);
+        fby = fbx;
+        fbx = t;
+        const float uu = fmaf(-q, fx, fy);
+        fy = fx;
+        fx = uu;
+        z++;
+    }
+    if (z & 1) { fby = -fby; fy = -fy; }
+    warp_reconverge(wmask);
+    const double bx = fbx, by = fby, x = fx, y = fy;
+    const double sq = (bx + by) * (bx + by) - bx * bx;   // exact: < 2^40
+    if (z == 0) {
+        o.u3 = by * by;
+        o.v3 = v - sq + o.u3;
+    } else {
+        const double dx = dexact_div(fma(bx, Dy, -w * x), By, rBy, err);
+        const double Q1 = dx * y;
+        const double dy0 = Q1 + Dy;
+        const double dy = dexact_div(dy0, x, rcp64(x), err);
+        o.v3 = G * (dy0 + Q1) - sq + by * by;
+        o.u3 = fma(by, by, -G * y * dy);
+    }
+    o.x = x;
+    o.y = y;
+    o.G = G;
+    return true;
+}
+
 // The giant step's composition (NUCOMPchoose, Alg. 4, for I1 = mu_1 and a reduced
 // I2 != mu_1) followed by the canonical representative (R17): returns
 // Q = |2 u3| and P* = s - ((s + v3) mod Q) in (s - Q, s] (P = -v3 mod Q, l.753).
@@ -484,15 +532,21 @@ struct GiantComp {
     float lg;
 };
 
+// dup_fast (a compile-time constant at each call site): squarings take the fp64
+// NUDUPL; otherwise (the giant kernel, where mu_1^2 is rare) the generic path.
 EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, i64 L,
-                               float sqrtd_f, int plain_th, u32 *err, u32 wmask) {
+                               float sqrtd_f, int plain_th, u32 *err, u32 wmask,
+                               bool dup_fast = false) {
     GiantComp r;
     const i64 Q1 = m1.Q, P1 = m1.P;
     if (P2 >= Q2) P2 -= Q2 * (i64)ffloor_div_pos((float)P2, (float)Q2);   // Alg. 4 l.739
-    const bool rare = Q1 <= plain_th || Q2 <= plain_th || (Q1 == Q2 && P1 == P2);
-    // lanes of `wmask` that run the NUCOMP fast path (its reconvergence points
-    // must be reached by exactly these lanes)
-    const u32 fmask = warp_ballot(wmask, !rare);
+    const bool dup = Q1 == Q2 && P1 == P2;
+    const bool rare = Q1 <= plain_th || Q2 <= plain_th || (dup && !dup_fast);
+    const bool fdup = dup_fast && dup && !rare;
+    // lanes of `wmask` that run the NUCOMP / NUDUPL fast paths (their
+    // reconvergence points must be reached by exactly these lanes)
+    const u32 fmask = warp_ballot(wmask, !rare && !fdup);
+    const u32 dmask = dup_fast ? warp_ballot(wmask, fdup) : 0u;
     if (rare) {
         const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
         r.Q = c.Q;
@@ -502,11 +556,17 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
         r.kind = c.kind;
         return r;
     }
-    const double dd = (double)d;
-    const double w2 = rint(((double)P2 * (double)P2 - dd) * rcp64(2.0 * (double)Q2));   // exact
     CompD o;
-    if (!nucomp_d((double)(Q1 >> 1), -(double)P1, (double)m1.w, (double)(Q2 >> 1), -(double)P2,
-                  w2, (float)L, o, err, fmask)) {
+    bool ok;
+    if (fdup) {
+        ok = nudupl_d((double)(Q1 >> 1), -(double)P1, (double)m1.w, (float)L, o, err, dmask);
+    } else {
+        const double dd = (double)d;
+        const double w2 = rint(((double)P2 * (double)P2 - dd) * rcp64(2.0 * (double)Q2));   // exact
+        ok = nucomp_d((double)(Q1 >> 1), -(double)P1, (double)m1.w, (double)(Q2 >> 1),
+                      -(double)P2, w2, (float)L, o, err, fmask);
+    }
+    if (!ok) {
         const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
         r.Q = c.Q;
         r.P = s - floor_mod(s - c.P, c.Q);
@@ -530,7 +590,7 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
         r.lg = log2_approx((float)o.G * mag / (float)Qd);
     else   // |N(gamma)| = (Q1/2)(Q2/2)/|u3|, use the conjugate (no cancellation)
         r.lg = log2_approx(2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1) / ((float)o.G * mag));
-    r.kind = 1;
+    r.kind = fdup ? 2u : 1u;
     if (((r.Q & 3) != 2) | ((r.P & 1) != 1) | (((i64)o.G & 1) == 0)) *err += 1;
     return r;
 }

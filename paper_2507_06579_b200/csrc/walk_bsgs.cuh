@@ -367,12 +367,14 @@ struct GiantInfo {
 
 // Advance: mu'_k = rho-reduce(NUCOMPchoose(mu_1, mu'_{k-1})) with its residue and
 // distance; no lookup.  *err counts invariant violations.
-EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmask = 0xffffffffu) {
+// dup_fast: the step is (normally) a squaring, mu'_k = mu_1^2 (the prep kernel)
+EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmask = 0xffffffffu,
+                               bool dup_fast = false) {
     GiantInfo gi;
     const i64 d = (i64)g.d;
     const i64 s = g.s;
     const GiantComp c = giant_compose(g.m1, (i64)g.Qc, (i64)g.Pc, d, s, (i64)g.L, g.sqrtd,
-                                      B.plain_th, err, wmask);
+                                      B.plain_th, err, wmask, dup_fast);
     warp_reconverge(wmask);
     gi.kind = c.kind;
     u32 t = mod3_small(g.t1 + g.tc + 3u - c.tg);   // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
@@ -436,7 +438,7 @@ EIS_HD int giant_hit(const GiantLane &g, int kind, u32 te, u32 t, float dist, u3
 // (R35) and enough margin, mu'_2 becomes the giant stride: mu''_1 = mu'_2 and
 // mu''_k = mu'_2 * mu''_{k-1}.  Same lane mask rules as giant_advance.
 EIS_HD GiantInfo giant_start(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmask = 0xffffffffu) {
-    const GiantInfo gi = giant_advance(g, B, err, wmask);
+    const GiantInfo gi = giant_advance(g, B, err, wmask, true);
     const float M2 = two_sided_margin2(g.d);
     // stride shorter than the arc by >= 2M (R35), and mu''_1 = mu_1^2 beyond the
     // window by >= M (so its direct hits are never trivial)
@@ -821,7 +823,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         const u32 amask = __ballot_sync(FULL_MASK, two && g.phase == PH_GIANT);
         if (two && g.phase == PH_GIANT) {
-            const GiantInfo gi = giant_advance(g, B, &err, amask);
+            const GiantInfo gi = giant_advance(g, B, &err, amask, true);   // mu''_1^2
             giant++;
             red += gi.nred;
         }

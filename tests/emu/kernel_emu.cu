@@ -6,6 +6,9 @@
 // usage: kernel_emu MODE ALPHA_X16 NB [PLAIN_TH [TWO_SIDED]] < d-list  (MODE: half | bsgs;
 //        NB: table buckets per d, 0 = sized from d; half mode: 99 = integer step)
 // prints per d: "d t baby giant reduce fallback err kinds(plain,comp,dupl)"
+// MODE dupl (ALPHA_X16 = ideals per d): squares the first ideals of the principal
+// cycle with NUDUPL twice, the generic int64 nudupl() and the fp64 nudupl_d(),
+// and prints per d: "d checked mismatches err" (outputs u3 v3 x y G compared).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -20,6 +23,36 @@ int main(int argc, char **argv) {
         return 2;
     }
     const bool bsgs = strcmp(argv[1], "bsgs") == 0;
+    if (strcmp(argv[1], "dupl") == 0) {
+        const int per_d = atoi(argv[2]);
+        const i64 plain_th = argc > 4 ? atoi(argv[4]) : 50;
+        unsigned long long dd;
+        while (scanf("%llu", &dd) == 1) {
+            u32 err = 0, r1;
+            int checked = 0, bad = 0;
+            BabyState st;
+            const i64 L = (i64)isqrt_u64_dev((u64)isqrt_u64_dev(dd));
+            if (!baby_init(st, dd, &r1)) {
+                for (int k = 0; k < per_d; k++) {
+                    if ((i64)st.Q > plain_th) {
+                        const Mu1Form m = mu1_form((i64)st.Q, (i64)st.P, (i64)dd, &err);
+                        i64 u3, v3, G, x, y;
+                        nudupl((i64)(m.Q >> 1), -(i64)m.P, m.w, L, u3, v3, G, x, y, &err);
+                        CompD o;
+                        nudupl_d((double)(m.Q >> 1), -(double)m.P, (double)m.w, (float)L, o, &err,
+                                 0xffffffffu);
+                        checked++;
+                        if ((i64)o.u3 != u3 || (i64)o.v3 != v3 || (i64)o.x != x || (i64)o.y != y ||
+                            (i64)o.G != G)
+                            bad++;
+                    }
+                    if (baby_step(st)) break;
+                }
+            }
+            printf("%llu %d %d %u\n", dd, checked, bad, err);
+        }
+        return 0;
+    }
     BsgsArgs B;
     const float alpha = atoi(argv[2]) / 16.0f;
     const int nb_fixed = atoi(argv[3]);
@@ -78,7 +111,7 @@ int main(int argc, char **argv) {
                     red += gi.nred;
                     kinds[gi.kind]++;
                     while (!giant_lookup(g, tab.data(), lst.data(), B)) {   // giant kernel
-                        gi = giant_advance(g, B, &err);
+                        gi = giant_advance(g, B, &err, 0xffffffffu, true);   // (squarings: fp64 NUDUPL)
                         giant++;
                         red += gi.nred;
                         kinds[gi.kind]++;

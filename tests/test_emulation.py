@@ -98,3 +98,19 @@ def test_verbatim_guard_case_661(emu):
     d=661; the guarded walk returns the oracle's t=2."""
     rows = run(emu, [661], "bsgs")
     assert rows[0, 1] == 2 == c_oracle.residue(661)
+
+
+def test_fp64_nudupl_matches_generic_nudupl(emu):
+    """The prep kernel's fp64 NUDUPL (forms.cuh nudupl_d, Alg. 3) gives
+    the same (u3, v3, x, y, G) as the generic int64 nudupl() on the first 64
+    ideals of the principal cycle of seeded d up to 1e11. Its cofactor yy comes
+    from the nearest-integer xgcd (R36) and is used only mod u/G."""
+    ds = np.concatenate([workloads.sample_candidates(lo, hi, 300, seed=11)
+                         for lo, hi in ((10**6, 10**7), (10**9, 2 * 10**9), (9 * 10**10, 10**11))])
+    out = subprocess.run([emu, "dupl", "64", "0"], input="\n".join(str(int(d)) for d in ds),
+                         capture_output=True, text=True, check=True).stdout
+    rows = np.array([[int(v) for v in ln.split()] for ln in out.splitlines()], dtype=np.int64)
+    assert len(rows) == len(ds)
+    assert rows[:, 1].sum() > 20000          # squarings compared
+    assert rows[:, 2].sum() == 0             # mismatches
+    assert rows[:, 3].sum() == 0             # invariant violations
