@@ -45,8 +45,8 @@ OPS_PER_GIANT = 700    # thread-instructions of one fast-path giant step (DESIGN
 OPS_PER_ENTRY = 12     # store insert per window entry: slot pack, hash, bucket insert
 # DRAM bytes per d of the BSGS walk at the bench configuration: dram__bytes_read +
 # dram__bytes_write of bsgs_window + bsgs_prep + bsgs_giant for one segment (ncu
-# --set full, profiles/r01_bsgs_walk.txt: 26.47 + 1.07 + 9.67 GB) / the segment's
-# 4.22 M d.  Algorithmic: list write + read-back 3.6 KB, table 2.9 KB, ~18.5 probes
+# --set full, profiles/r01_bsgs_walk.txt: 39.73 + 1.60 + 14.49 GB) / the segment's
+# 6.33 M d.  Algorithmic: list write + read-back 3.6 KB, table 2.9 KB, ~18.5 probes
 # x 64 B, records ~0.2 KB = ~7.9 KB per d.
 BSGS_DRAM_BYTES_PER_D = 8810
 
