@@ -262,14 +262,28 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         const BsgsSizes za = bsgs_sizes(d_a, alpha_for(d_a) / 16.0f, g.two_sided);
         const BsgsSizes zb = bsgs_sizes(d_b, alpha_for(d_b) / 16.0f, g.two_sided);
         const int lcap = std::max(za.lcap, zb.lcap), nbk = std::max(za.nb, zb.nb);
-        for (SegBuf &b : g.buf) {
-            if (b.bsgs.lists && b.bsgs.lists_n >= seg_cap * (size_t)lcap &&
-                b.bsgs.tables_n >= seg_cap * (size_t)nbk * BKT && b.bsgs.brecs_n >= seg_cap)
-                continue;
-            CUDA_TRY(cudaStreamSynchronize(g.aux));
-            CUDA_TRY(cudaStreamSynchronize(s));
-            if (bsgs_reserve(b.bsgs, (size_t)seg_cap, lcap, nbk))
-                return fail(EIS_ENOMEM, "BSGS scratch allocation failed");
+        // if the device cannot hold two buffers of bsgs_gb, halve the segment
+        // (results do not depend on it) down to 2^16 candidates
+        for (;;) {
+            bool ok = true;
+            for (SegBuf &b : g.buf) {
+                if (b.bsgs.lists && b.bsgs.lists_n >= seg_cap * (size_t)lcap &&
+                    b.bsgs.tables_n >= seg_cap * (size_t)nbk * BKT && b.bsgs.brecs_n >= seg_cap)
+                    continue;
+                CUDA_TRY(cudaStreamSynchronize(g.aux));
+                CUDA_TRY(cudaStreamSynchronize(s));
+                if (bsgs_reserve(b.bsgs, (size_t)seg_cap, lcap, nbk)) {
+                    ok = false;
+                    break;
+                }
+            }
+            if (ok) break;
+            (void)cudaGetLastError();                    // clear the allocation failure
+            for (SegBuf &b : g.buf) bsgs_free(b.bsgs);
+            if (seg_cap <= (1ull << 16)) return fail(EIS_ENOMEM, "BSGS scratch allocation failed");
+            const u64 total = i_last - i_first + 1;
+            const u64 nseg = (total + seg_cap / 2 - 1) / (seg_cap / 2);
+            seg_cap = std::max<u64>((total + nseg - 1) / nseg, 1ull << 16);
         }
     }
     CUDA_TRY(cudaEventRecord(g.ev[2], s));

@@ -310,3 +310,29 @@ def test_secondary_term_fits():
     # residue classes t = 1 and t = 2 are equally frequent (to 1%)
     T2 = R["D"].astype(np.int64) - R["E"].astype(np.int64) - R["T1"].astype(np.int64)
     assert abs(int(R["T1"][-1]) - int(T2[-1])) < 0.01 * int(T2[-1])
+
+
+@pytest.mark.gpu
+def test_bsgs_scratch_shrinks_under_memory_pressure():
+    """With most of the device held by another allocation, the BSGS scratch (two
+    buffers of bsgs_gb = 48 GiB by default) does not fit: the library halves its
+    segments instead of failing, and the Table 1 window (9.9e9, 1e10]
+    (E = 3,334,227) comes out unchanged."""
+    import torch
+    eis.init(0)                                   # (re-init frees the library's scratch)
+    old = eis.get_option("bsgs_gb")
+    eis.set_option("bsgs_gb", 48)
+    free, _ = torch.cuda.mem_get_info(0)
+    hold = None
+    try:
+        # leave 40 GiB: the range's two segments need 2 x ~31 GB of scratch;
+        # halved segments (2 x ~16 GB) fit
+        keep = 40 << 30
+        if free > keep + (1 << 30):
+            hold = torch.empty(free - keep, dtype=torch.uint8, device="cuda:0")
+        D, E = eis.count_window(9_900_000_000, [10_000_000_000])
+        assert int(E[0]) == 3_334_227
+    finally:
+        del hold
+        torch.cuda.empty_cache()
+        eis.set_option("bsgs_gb", old)
