@@ -152,7 +152,8 @@ EIS_HD u32 conj_P(u32 Q, u32 P, u32 s) {     // = floor((s + P)/Q) Q - P (a rho 
 // Entry jj >= 1 holds (Q_j, P_j) with P_j^2 = d - Q_{j-1} Q_j, P_j > 0 on reduced
 // ideals, so Q_{j-1} identifies P_j; entry 0 is (2, P_1) = O, the only reduced
 // ideal with Q = 2 (self-conjugate).
-EIS_HD_COLD int match_kind(u64 d, u32 Q, u32 P, u32 s, u32 jj, u32 Qprev) {   // (rare)
+// (inline: a call ran on nearly every giant iteration, a key match in some lane)
+EIS_HD int match_kind(u64 d, u32 Q, u32 P, u32 s, u32 jj, u32 Qprev) {
     if (jj == 0) return HIT_DIRECT;
     const u64 nrm = d - (u64)Qprev * Q;
     if ((u64)P * P == nrm) return HIT_DIRECT;
@@ -853,7 +854,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #define GIANT_THREADS 128
 #endif
 #ifndef GIANT_MINB
-#define GIANT_MINB 8                          // 64 registers: 7 / 8 CTAs per SM measured 394.4 / 395.6 M d/s (earlier: 5 / 6 / 7 -> 345 / 354 / 358)
+#define GIANT_MINB 7                          // 72 registers; with match_kind inlined 7 / 8 CTAs per SM measured 406.4 / 401.0 M d/s (8 spills more)
 #endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
