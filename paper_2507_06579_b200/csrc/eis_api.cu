@@ -55,9 +55,9 @@ struct Ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // options
     int mode = EIS_MODE_AUTO;
-    u64 crossover = 2500000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
-                                     // HALF 1.06x faster at 2e9, BSGS 1.07x at 3e9, 1.16x
-                                     // at 4e9, 1.46x at 1e10, 2.5x at 1e11)
+    u64 crossover = 2100000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
+                                     // HALF 1.01x faster at 2e9, tie at 2.1e9, BSGS 1.10x at
+                                     // 3e9, 1.49x at 1e10, 2.6x at 1e11)
     int alpha_x16 = 0;               // BSGS baby window W = alpha d^(1/4); 0 = by d (alpha_for)
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
@@ -209,8 +209,9 @@ int alpha_for(u64 d) {
     if (g.alpha_x16 > 0) return g.alpha_x16;
     const double x = std::log10((double)d);
     double a;
-    if (x <= 9.7) a = 32;                                  // 2.0
-    else if (x <= 10.0) a = 32 + (28 - 32) * (x - 9.7) / 0.3;
+    if (x <= 9.6) a = 32;                                  // 2.0
+    else if (x <= 9.7) a = 32 + (28 - 32) * (x - 9.6) / 0.1;
+    else if (x <= 10.0) a = 28;                            // 1.75
     else if (x <= 10.5) a = 28 + (24 - 28) * (x - 10.0) / 0.5;
     else a = 24;
     return (int)std::lround(a);
