@@ -48,7 +48,7 @@ OPS_PER_ENTRY = 12     # store insert per window entry: slot pack, hash, bucket 
 # --set full, profiles/r01_bsgs_walk.txt: 39.73 + 1.59 + 13.72 GB) / the segment's
 # 6.33 M d.  Algorithmic: list write + read-back 3.6 KB, table 2.9 KB, ~18.5 probes
 # x 64 B, records ~0.2 KB = ~7.9 KB per d.
-BSGS_DRAM_BYTES_PER_D = 8690
+BSGS_DRAM_BYTES_PER_D = 8563
 
 
 def _env_int(k, d):
@@ -347,11 +347,11 @@ def main():
                 "bound": "alu", "kernel": dom_name,
                 "achieved": achieved, "peak": peak, "unit": "Tops/s", "frac": achieved / peak,
                 "traffic": BSGS_DRAM_BYTES_PER_D * nD_rank if bsgs else 50.8e6,
-                "traffic_note": ("dram read+write bytes per step of the BSGS walk: 8.69 KB per d "
+                "traffic_note": ("dram read+write bytes per step of the BSGS walk: 8.56 KB per d "
                                  "measured by ncu --set full on the bench workload "
                                  "(profiles/r01_bsgs_walk.txt) x d per step; algorithmic ~7.9 KB "
                                  "per d (list 3.6, table 2.9, probes 1.2, records 0.2); the "
-                                 "walk is issue/latency-bound at ~2.8 TB/s average") if bsgs else
+                                 "walk is issue/latency-bound at ~3.0 TB/s average") if bsgs else
                                 "dram read+write bytes per walk launch, ncu --set full "
                                 "(profiles/r01_half_walk.txt); algorithmic bytes = 4 per d "
                                 "(survivor list) = 50.7 MB",

@@ -55,9 +55,9 @@ struct Ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // options
     int mode = EIS_MODE_AUTO;
-    u64 crossover = 2100000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
-                                     // HALF 1.01x faster at 2e9, tie at 2.1e9, BSGS 1.10x at
-                                     // 3e9, 1.49x at 1e10, 2.6x at 1e11)
+    u64 crossover = 1600000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
+                                     // HALF 1.02x faster at 1.4e9, BSGS 1.02x at 1.6e9,
+                                     // 1.19x at 3e9, 1.61x at 1e10, 2.8x at 1e11)
     int alpha_x16 = 0;               // BSGS baby window W = alpha d^(1/4); 0 = by d (alpha_for)
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
@@ -203,17 +203,16 @@ bool cand_range(u64 lo, u64 hi, u64 &i_first, u64 &i_last) {
 }
 
 // BSGS window factor (x16) for a segment ending at d: the option, or (0) the
-// measured optimum log-interpolated over d (2.25 at 5e9, 1.75 at
-// 1e10, 1.5 at 1e11); results never depend on it (R6, R29)
+// measured optimum log-interpolated over d (2.25 up to 2e9, 1.875
+// at 1e10, 1.625 at 1e11); results never depend on it (R6, R29)
 int alpha_for(u64 d) {
     if (g.alpha_x16 > 0) return g.alpha_x16;
     const double x = std::log10((double)d);
     double a;
-    if (x <= 9.6) a = 32;                                  // 2.0
-    else if (x <= 9.7) a = 32 + (28 - 32) * (x - 9.6) / 0.1;
-    else if (x <= 10.0) a = 28;                            // 1.75
-    else if (x <= 10.5) a = 28 + (24 - 28) * (x - 10.0) / 0.5;
-    else a = 24;
+    if (x <= 9.3) a = 36;                                  // 2.25
+    else if (x <= 10.0) a = 36 + (30 - 36) * (x - 9.3) / 0.7;
+    else if (x <= 11.0) a = 30 + (26 - 30) * (x - 10.0);
+    else a = 26;
     return (int)std::lround(a);
 }
 

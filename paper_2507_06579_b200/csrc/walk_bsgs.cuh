@@ -575,9 +575,47 @@ __device__ __forceinline__ void flush_stats(const WalkArgs &a, u64 baby, u64 gia
 // Shared memory per warp: the table (nb * BKT slots) and nb fill counters.
 EIS_HD u32 window_smem_words(u32 nb) { return nb * BKT + ((nb + 3) & ~3u); }
 
+// L2 policy of the window kernel (WIN_L2HINT bits): 2 = the build's list loads
+// evict_first (a list is dead in L2 once its store is built; the giant kernel
+// reads only the few entries a key match needs), 4 = the table write-out
+// evict_first (read only by the next kernel's probes).  With both, L2 keeps
+// more of the lists still waiting for their build: +3% on the bench line
+// (loads alone -0.6%, tables alone +0.8%; list stores evict_last -1.6%).
+// WIN_ST256: one 32-byte store (st.global.v8, sm_100) per 8 entries instead
+// of two 16-byte stores: +3.7%.
+#ifndef WIN_L2HINT
+#define WIN_L2HINT 6
+#endif
+#ifndef WIN_ST256
+#define WIN_ST256 1
+#endif
+__device__ __forceinline__ u64 l2_policy_first() {
+    u64 p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void store_block(u32 *dst, const u32 (&e)[8]) {
+#if WIN_ST256
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"l"(dst), "r"(e[0]), "r"(e[1]), "r"(e[2]), "r"(e[3]), "r"(e[4]), "r"(e[5]),
+                   "r"(e[6]), "r"(e[7]) : "memory");
+#else
     reinterpret_cast<uint4 *>(dst)[0] = make_uint4(e[0], e[1], e[2], e[3]);
     reinterpret_cast<uint4 *>(dst)[1] = make_uint4(e[4], e[5], e[6], e[7]);
+#endif
+}
+
+// a list group load of the build (16 bytes)
+__device__ __forceinline__ uint4 list_ld4(const uint4 *p) {
+#if (WIN_L2HINT & 2)
+    uint4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_policy_first()));
+    return v;
+#else
+    return *p;
+#endif
 }
 
 __device__ __forceinline__ u32 smem_atom_inc(u32 addr) {
@@ -604,7 +642,7 @@ __device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[B
 #pragma unroll
     for (int k = 0; k < BUILD_K; k++) {
         const u32 i4 = (u32)(32 * k + lane);
-        nx[k] = (lst && i4 < n4) ? l4[i4] : make_uint4(0, 0, 0, 0);
+        nx[k] = (lst && i4 < n4) ? list_ld4(l4 + i4) : make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -627,7 +665,7 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
 #pragma unroll
             for (int k = 0; k < K; k++) {
                 const u32 i4 = jb / 4 + (u32)(32 * K + 32 * k + lane);
-                nx[k] = i4 < n4 ? l4[i4] : make_uint4(0, 0, 0, 0);
+                nx[k] = i4 < n4 ? list_ld4(l4 + i4) : make_uint4(0, 0, 0, 0);
             }
         } else {
             load_group0(lst_next, n, nx);            // the next d's first group
@@ -676,8 +714,13 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) {
+#if (WIN_L2HINT & 4)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                     ::"l"(dst), "r"(tab_s), "r"(nb * BKT * 4u), "l"(l2_policy_first()) : "memory");
+#else
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                      ::"l"(dst), "r"(tab_s), "r"(nb * BKT * 4u) : "memory");
+#endif
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
@@ -688,7 +731,7 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
 }
 
 #ifndef WINDOW_MINB
-#define WINDOW_MINB 5
+#define WINDOW_MINB 4                         // with the L2 hints: 3 / 4 / 5 / 6 CTAs per SM 436 / 436 / 433 / 427 M d/s
 #endif
 __global__ void __launch_bounds__(256, WINDOW_MINB)
 bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
@@ -856,6 +899,9 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #ifndef GIANT_MINB
 #define GIANT_MINB 7                          // 72 registers; with match_kind inlined 7 / 8 CTAs per SM measured 406.4 / 401.0 M d/s (8 spills more)
 #endif
+#ifndef GIANT_L2HINT
+#define GIANT_L2HINT 0                        // 1: table probes evict_first (-1%)
+#endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
 bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
@@ -938,8 +984,14 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 const u32 dst = (u32)__cvta_generic_to_shared(&pbuf[threadIdx.x][0]);
 #pragma unroll
                 for (int q = 0; q < 4; q++)
+#if GIANT_L2HINT
+                    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+                                 ::"r"(dst + 16 * q), "l"(src + 4 * q), "l"(l2_policy_first())
+                                 : "memory");
+#else
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q),
                                  "l"(src + 4 * q) : "memory");
+#endif
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
             const GiantInfo gi = giant_advance(g, B, &err, gmask);
