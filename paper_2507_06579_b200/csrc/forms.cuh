@@ -52,6 +52,15 @@ EIS_HD i64 floor_mod(i64 a, i64 b) {   // b > 0, result in [0, b)
     return a - floor_div(a, b) * b;
 }
 
+// exact floor-mod of fp64 integers, |a| < 2^52, 0 < b < 2^52 (rb ~ 1/b)
+EIS_HD double dfloor_mod(double a, double b, double rb) {   // b > 0, result in [0, b)
+    const double q = floor(a * rb);
+    double r = fma(-q, b, a);
+    r = r < 0.0 ? r + b : r;                  // selects, not branches
+    r = r >= b ? r - b : r;
+    return r;
+}
+
 // 32-bit floor division for 0 <= a < 2^23, 0 < b < 2^23 (same float trick as
 // the baby step: round(a/b) by one FFMA, then one correction).
 EIS_HD u32 udiv23(u32 a, u32 b) {
@@ -304,6 +313,21 @@ EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
     const i64 a1 = Q1 >> 1, a2 = Q2 >> 1;
     i64 x, y;
     const i64 e = xgcd(a1, a2, x, y);         // x a1 + y a2 = e
+    Composed r;
+    r.tg = 0;                                  // gamma = S odd
+    r.kind = 0;
+    if (e == 1) {
+        // coprime norms (the usual case): S = 1 with (X, Y) = (1, 0), so
+        // b3 = x a1 P2 + y a2 P1 mod 2 a1 a2 (the CRT lift).  min(a1, a2) <= 25
+        // bounds |x a1|, |y a2| by 25 * 2^19 and P1, P2 < 2^20, so the sum is an
+        // exact fp64 integer < 2^45 and one exact floor-mod finishes it.
+        const double M = 2.0 * (double)a1 * (double)a2;
+        const double v = fma((double)(x * a1), (double)P2, (double)(y * a2) * (double)P1);
+        r.Q = 2 * a1 * a2;
+        r.P = (i64)dfloor_mod(v, M, rcp64(M));
+        r.lg = 0.f;
+        return r;
+    }
     const i64 n = (P1 + P2) / 2;
     i64 X, Y;
     const i64 S = xgcd_s(e, n, X, Y);         // X e + Y n = S
@@ -319,12 +343,9 @@ EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
     const i64 t3 = mulmod(floor_mod(Y, M), h, M);
     const i64 num = floor_mod(t1 + t2 + t3, M);
     if (num % S != 0) *err += 1;
-    Composed r;
     r.Q = 2 * a3;
     r.P = num / S;                             // in [0, 2 a3)
-    r.tg = 0;                                  // gamma = S odd
     r.lg = log2_approx((float)S);
-    r.kind = 0;
     return r;
 }
 
@@ -379,13 +400,6 @@ EIS_HD double dexact_div(double n, double dv, double rdv, u32 *err) {
     const double q = rint(n * rdv);
     if (fma(-q, dv, n) != 0.0) *err += 1;
     return q;
-}
-EIS_HD double dfloor_mod(double a, double b, double rb) {   // b > 0, result in [0, b)
-    const double q = floor(a * rb);
-    double r = fma(-q, b, a);
-    r = r < 0.0 ? r + b : r;                  // selects, not branches
-    r = r >= b ? r - b : r;
-    return r;
 }
 
 struct CompD {

@@ -61,12 +61,24 @@ struct BsgsArgs {
     int j1;             // entry index of mu_1 (= 7 mod 8: the end of a block)
     int nb;             // table buckets per d
     int lcap;           // list stride per d (>= nw, multiple of 32)
-    int plain_th;       // Alg. 4 plain-product threshold on Q (paper: 50)
+    int plain_th;       // Alg. 4 plain-product threshold on Q (paper: 50; kernels: PLAIN_TH)
     float giant_cap_mul;// giant-step cap = giant_cap_mul * (d^(1/4) + 10)
     int two_sided;      // R35: conjugate hits + doubled stride (0 = the paper's one-sided Alg. 1)
 };
 
 EIS_HD u32 mod3(u32 v) { return v % 3u; }
+EIS_HD int __double2loint_hd(double x) {          // the low 32 bits of x's encoding
+#ifdef __CUDA_ARCH__
+    return __double2loint(x);
+#else
+    u64 b;
+    memcpy(&b, &x, sizeof b);
+    return (int)(u32)b;
+#endif
+}
+#ifndef RHO_CARRY_C
+#define RHO_CARRY_C 1                 // giant_advance's rho loop carries C = (d - P^2)/Q
+#endif
 EIS_HD u32 mod3_small(u32 v) { return v - 3u * ((v * 0x5556u) >> 16); }   // v < 2^15
 
 // Two-sided window (R35).  Conjugation reverses the principal cycle
@@ -302,6 +314,31 @@ EIS_HD u32 win_step(WinLane &w) {
     return list_entry(f_to_u(w.st.Q), w.st.t2 >> 1);
 }
 
+// WIN_DEFER_EXIT: the lockstep loop only records in which step of an 8-step
+// block a symmetry exit fired (one bit per step); the result is derived after
+// the block from the entries (baby_result_f in terms of list entries: t of the
+// exit step k and of k - 1 and whether their Q agree, R13).  Capturing it per
+// step cost ~10 predicated instructions per step.
+#ifndef WIN_DEFER_EXIT
+#define WIN_DEFER_EXIT 0
+#endif
+EIS_HD u32 win_step_x(WinLane &w, bool &ex) {
+    ex = baby_step_fd(w.st, w.sqd_m, w.prod);
+    return list_entry(f_to_u(w.st.Q), w.st.t2 >> 1);
+}
+// exit at the first set bit k of exk; prev = the entry before e[0]
+EIS_HD void win_exit(WinLane &w, const u32 (&e)[8], u32 prev, u32 exk) {
+    const u32 k = (u32)__builtin_ctz_portable(exk);
+    u32 cur = e[0];
+#pragma unroll
+    for (int i = 1; i < 8; i++) {
+        if ((u32)i == k) { prev = e[i - 1]; cur = e[i]; }
+    }
+    const u32 tk = cur >> 20, tp = prev >> 20;
+    w.res = ((cur ^ prev) & 0xFFFFFu) == 0 ? tk + tp : 2u * tp;
+    w.live = false;
+}
+
 // fold the pending multipliers into the distance (every 4 steps: entry j = 3 mod 4)
 EIS_HD void win_flush(WinLane &w) {
     w.dist += log2_approx(w.prod);
@@ -383,6 +420,48 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
     i64 Q = c.Q, P = c.P;                        // P canonical in (s - Q, s]
     u32 nred = 0;
     if (Q - P > s) {                             // not reduced (R18): apply rho
+#if RHO_CARRY_C
+        // Exact fp64 integers, carrying the third coefficient C = (d - P^2)/Q of
+        // the ideal (Q, P) so that no step forms d - P'^2 (|P'| reaches 2^28, so
+        // that needs int64): rho gives P' = qQ - P, Q' = C + q (P - P'), C' = Q,
+        // and moving P' to its canonical representative P' + kQ' gives
+        // C' - k (P' + P'_c).  Every result is an integer below 2^38 and each
+        // product is inside an fma (one rounding of an exact value), so all
+        // of it is exact even where k (P' + P'_c) itself exceeds 2^53.  The residue bit
+        // of P' is read from the low word of P' + 1.5 * 2^52 (no conversion), and
+        // the distance is accumulated as a product, with one log at the end.
+        const double sd = (double)s;
+        double Qd = (double)Q, Pd = (double)P, rQ = rcp64(Qd);
+        // C = (d - P^2)/Q: |P| < Q + s may reach 2^28, so d - P^2 in int64; the
+        // quotient is < 2^37 and the division exact, so rint recovers it
+        double Cd = rint((double)(d - P * P) * rQ);
+        double mag = 1.0;                               // prod |P' + sqrt d| / Q
+        do {
+            const double num = Pd + sd;
+            double q = floor(num * rQ);              // floor((P + sqrt d)/Q)
+            const double rr = fma(-q, Qd, num);
+            q = rr < 0.0 ? q - 1.0 : (rr >= Qd ? q + 1.0 : q);
+            const double Pn = fma(q, Qd, -Pd);
+            double Qn = fma(q, Pd - Pn, Cd);
+            const u32 plo = (u32)__double2loint_hd(Pn + 6755399441055744.0);   // P' mod 2^32
+            t = mod3_small(t + 1u + ((plo >> 1) & 1u));
+            mag *= fabs(Pn + (double)g.sqrtd) * rQ;
+            Cd = Qd;                                  // C' = Q
+            if (Qn < 0.0) { Qn = -Qn; Cd = -Cd; }     // the ideal of norm |Q'|
+            Qd = Qn;
+            rQ = rcp64(Qd);
+            // canonical P in (s - Q, s]: P_c = P' + k Q with k = floor((s - P')/Q)
+            const double a = sd - Pn;
+            double k = floor(a * rQ);
+            const double r = fma(-k, Qd, a);
+            k = r < 0.0 ? k - 1.0 : (r >= Qd ? k + 1.0 : k);
+            Pd = fma(k, Qd, Pn);
+            Cd = fma(-k, Pn + Pd, Cd);
+            if (++nred > 4096) { *err += 1; break; }
+        } while (Qd - Pd > sd);
+        dist += log2_approx((float)mag);
+        if (fma(Qd, Cd, Pd * Pd) != (double)d) *err += 1;   // d = P^2 + Q C, exact (< 2^40)
+#else
         // exact fp64 integers (|P|, Q < 2^32); Q' = (d - P'^2)/Q with d - P'^2 in int64
         const double sd = (double)s;
         double Qd = (double)Q, Pd = (double)P, rQ = rcp64(Qd);
@@ -403,6 +482,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
             Pd = sd - dfloor_mod(sd - Pn, Qd, rQ);   // canonical P in (s - Q, s]
             if (++nred > 4096) { *err += 1; break; }
         } while (Qd - Pd > sd);
+#endif
         Q = (i64)Qd;
         P = (i64)Pd;
     }
@@ -618,6 +698,17 @@ __device__ __forceinline__ uint4 list_ld4(const uint4 *p) {
 #endif
 }
 
+// WIN_LD256: the build reads 8 entries per lane with one 32-byte load, which
+// also takes the evict_first priority as a plain qualifier (no createpolicy).
+#ifndef WIN_LD256
+#define WIN_LD256 0
+#endif
+__device__ __forceinline__ void list_ld8(const u32 *p, uint4 &a, uint4 &b) {
+    asm volatile("ld.global.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
+                   "=r"(b.w) : "l"(p));
+}
+
 __device__ __forceinline__ u32 smem_atom_inc(u32 addr) {
     u32 old;
     asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(addr) : "memory");
@@ -637,6 +728,11 @@ __device__ __forceinline__ void smem_st4_zero(u32 addr) {
 // nb fill counters, both zero on entry and on exit) and written to dst.
 __device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[BUILD_K]) {
     const int lane = threadIdx.x & 31;
+#if WIN_LD256
+    static_assert(BUILD_K == 2, "WIN_LD256 loads 8 entries per lane per group");
+    nx[0] = nx[1] = make_uint4(0, 0, 0, 0);
+    if (lst && 8u * (u32)lane < n) list_ld8(lst + 8 * lane, nx[0], nx[1]);
+#else
     const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
     const u32 n4 = (n + 3) >> 2;
 #pragma unroll
@@ -644,6 +740,7 @@ __device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[B
         const u32 i4 = (u32)(32 * k + lane);
         nx[k] = (lst && i4 < n4) ? list_ld4(l4 + i4) : make_uint4(0, 0, 0, 0);
     }
+#endif
 }
 
 // nx: this d's first list group on entry (the caller or the previous call loaded
@@ -654,19 +751,27 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
                                             u32 n, u32 nb, u32 tab_s, u32 cnt_s,
                                             u32 *__restrict__ dst, uint4 (&nx)[BUILD_K]) {
     const int lane = threadIdx.x & 31;
+#if !WIN_LD256
     const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
     const u32 n4 = (n + 3) >> 2;
+#endif
     constexpr int K = BUILD_K;                       // 16-byte loads per lane per group
     for (u32 jb = 0; jb < n; jb += 128 * K) {
         uint4 cur[K];
 #pragma unroll
         for (int k = 0; k < K; k++) cur[k] = nx[k];
         if (jb + 128 * K < n) {
+#if WIN_LD256
+            const u32 j8 = jb + 128 * K + 8u * (u32)lane;
+            nx[0] = nx[1] = make_uint4(0, 0, 0, 0);
+            if (j8 < n) list_ld8(lst + j8, nx[0], nx[1]);
+#else
 #pragma unroll
             for (int k = 0; k < K; k++) {
                 const u32 i4 = jb / 4 + (u32)(32 * K + 32 * k + lane);
                 nx[k] = i4 < n4 ? list_ld4(l4 + i4) : make_uint4(0, 0, 0, 0);
             }
+#endif
         } else {
             load_group0(lst_next, n, nx);            // the next d's first group
         }
@@ -679,7 +784,11 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
 #pragma unroll
             for (int w = 0; w < 4; w++) {
                 const int i = 4 * k + w;
+#if WIN_LD256
+                const u32 j = jb + 8 * lane + 4 * k + w;
+#else
                 const u32 j = jb + 128 * k + 4 * lane + w;
+#endif
                 const u32 e = w == 0 ? cur[k].x : (w == 1 ? cur[k].y : (w == 2 ? cur[k].z : cur[k].w));
                 const u32 key = entry_key(e);
                 sv[i] = slot_entry(key, j);
@@ -768,11 +877,26 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         u32 *lst = o.lists + (u64)idx * B.lcap;
         if (w.live) baby += 7;                           // theta_2 (closed form) + 6
+#if WIN_DEFER_EXIT
+        {
+            u32 exk = 0;
+#pragma unroll
+            for (int k = 2; k < 8; k++) {
+                bool ex;
+                e[k] = win_step_x(w, ex);
+                exk |= (u32)ex << k;
+                if (k == 3 || k == 7) win_flush(w);
+            }
+            if (__any_sync(FULL_MASK, w.live && exk != 0))
+                if (w.live && exk != 0) win_exit(w, e, 0u, exk);
+        }
+#else
 #pragma unroll
         for (int k = 2; k < 8; k++) {
             e[k] = win_step(w);
             if (k == 3 || k == 7) win_flush(w);
         }
+#endif
         if (w.live) {
             store_block(lst, e);
             if (B.j1 == 7) win_mark_mu1(w);
@@ -780,11 +904,25 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         for (int blk = 1; blk < nblk; blk++) {
             if (!__any_sync(FULL_MASK, w.live)) break;
             if (w.live) baby += 8;
+#if WIN_DEFER_EXIT
+            const u32 elast = e[7];
+            u32 exk = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                bool ex;
+                e[k] = win_step_x(w, ex);
+                exk |= (u32)ex << k;
+                if (k == 3 || k == 7) win_flush(w);
+            }
+            if (__any_sync(FULL_MASK, w.live && exk != 0))
+                if (w.live && exk != 0) win_exit(w, e, elast, exk);
+#else
 #pragma unroll
             for (int k = 0; k < 8; k++) {
                 e[k] = win_step(w);
                 if (k == 3 || k == 7) win_flush(w);
             }
+#endif
             if (w.live) {
                 store_block(lst + blk * 8, e);
                 if (blk * 8 + 7 == B.j1) win_mark_mu1(w);
@@ -899,6 +1037,16 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #ifndef GIANT_MINB
 #define GIANT_MINB 7                          // 72 registers; with match_kind inlined 7 / 8 CTAs per SM measured 406.4 / 401.0 M d/s (8 spills more)
 #endif
+#ifndef PLAIN_TH
+// Alg. 4 l.742: the plain product for Q <= 50 (R6).  NUCOMP in exact fp64
+// cannot take its place: threshold 0 gave invariant violations at 5e10 (the
+// "can overflow" of l.733: w of a small-norm form is ~d/Q).  The coprime case
+// of the plain product is a one-line CRT lift (forms.cuh plain_product).
+#define PLAIN_TH 50
+#endif
+#ifndef GIANT_DUP_FAST
+#define GIANT_DUP_FAST 0                      // 1: squarings in the giant kernel take nudupl_d
+#endif
 #ifndef GIANT_L2HINT
 #define GIANT_L2HINT 0                        // 1: table probes evict_first (-1%)
 #endif
@@ -994,7 +1142,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #endif
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
-            const GiantInfo gi = giant_advance(g, B, &err, gmask);
+            const GiantInfo gi = giant_advance(g, B, &err, gmask, GIANT_DUP_FAST != 0);
             giant++;
             red += gi.nred;
             asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1147,7 +1295,7 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     B.j1 = z.j1;
     B.nb = z.nb;
     B.lcap = z.lcap;
-    B.plain_th = 50;
+    B.plain_th = PLAIN_TH;
     B.giant_cap_mul = (float)giant_cap;
     B.two_sided = two_sided;
     if (bsgs_reserve(scr, (size_t)seg_len, z.lcap, z.nb)) return -3;

@@ -30,7 +30,7 @@ def emu(tmp_path_factory):
     return exe
 
 
-def run(exe, ds, mode, alpha_x16=16, ns_log2=0, plain_th=50, two_sided=1):
+def run(exe, ds, mode, alpha_x16=16, ns_log2=0, plain_th=0, two_sided=1):   # 0 = PLAIN_TH
     out = subprocess.run([exe, mode, str(alpha_x16), str(ns_log2), str(plain_th), str(two_sided)],
                          input="\n".join(str(int(d)) for d in ds), capture_output=True,
                          text=True, check=True).stdout
@@ -68,7 +68,7 @@ def test_bsgs_samples_at_scale(emu, scale, two_sided):
     assert rows[:, 3].sum() > 0                                  # giant steps were taken
 
 
-@pytest.mark.parametrize("alpha_x16,plain_th", [(4, 50), (64, 50), (16, 0), (16, 200)])
+@pytest.mark.parametrize("alpha_x16,plain_th", [(4, 0), (64, 0), (16, 50), (16, 200)])
 def test_bsgs_results_independent_of_alpha_and_threshold(emu, alpha_x16, plain_th):
     """Reading R6/R29: neither the baby window nor the plain-product threshold
     changes any result (only step counts and magnitudes)."""
