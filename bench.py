@@ -43,6 +43,12 @@ OPS_PER_BABY = 14
 GENERIC_PER_BABY = 34
 OPS_PER_GIANT = 700    # thread-instructions of one fast-path giant step (K3 BSGS)
 OPS_PER_ENTRY = 12     # store insert per window entry: slot pack, hash, bucket insert
+# algorithmic HBM bytes of the window kernel (per-unit figures): per
+# entry 4 (list write) + 4 (list read-back by the build) + 64 / (16 * 0.62) (table
+# slots at load 0.62 in 64-byte buckets); per d 32 (window record) + 4 + 4 (offset,
+# queue entry)
+WIN_BYTES_PER_ENTRY = 4 + 4 + 64 / (16 * 0.62)
+WIN_BYTES_PER_D = 40
 # DRAM bytes per d of the BSGS walk at the bench configuration: dram__bytes_read +
 # dram__bytes_write of bsgs_window + bsgs_prep + bsgs_giant for one segment (ncu
 # --set full, profiles/r01_bsgs_walk.txt: 39.73 + 1.59 + 13.72 GB) / the segment's
@@ -113,6 +119,16 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_hbm_gbs() -> float:
+    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the
+    B200_PROFILING.md fallback of 6,650 GB/s."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0
 
 
 def host_cores() -> int:
@@ -310,6 +326,17 @@ def main():
                 per_kernel[k]["frac"] = per_kernel[k]["tops"] / peak
         per_kernel["sieve"] = {"ms": kms["sieve"]}
         if bsgs:
+            # the window kernel is bound by HBM, not issue: its algorithmic bytes over
+            # its live span (which overlaps the giant kernel of the previous segment)
+            wbytes = WIN_BYTES_PER_ENTRY * entries + WIN_BYTES_PER_D * stats["d_classified"]
+            hbm_peak = measured_hbm_gbs()
+            per_kernel["window"]["hbm"] = {
+                "bytes_per_step": wbytes, "gbs": wbytes / (kms["window"] / 1e3) / 1e9,
+                "peak_gbs": hbm_peak, "frac": wbytes / (kms["window"] / 1e3) / 1e9 / hbm_peak,
+                "note": "live span includes the overlapped giant kernel; ncu alone "
+                        "(profiles/r01_bsgs_walk.txt): 39.7 GB in 7.22 ms per 6.33 M-d "
+                        "segment = 5.5 TB/s, 0.84 of the measured copy bandwidth"}
+        if bsgs:
             # the BSGS kernels run on two streams and overlap (the giant kernel of one
             # segment with the window kernel of the next), so the walk is the unit:
             # all of its algorithmic ops over its device time
@@ -349,9 +376,10 @@ def main():
                 "traffic": BSGS_DRAM_BYTES_PER_D * nD_rank if bsgs else 50.8e6,
                 "traffic_note": ("dram read+write bytes per step of the BSGS walk: 8.56 KB per d "
                                  "measured by ncu --set full on the bench workload "
-                                 "(profiles/r01_bsgs_walk.txt) x d per step; algorithmic ~7.9 KB "
-                                 "per d (list 3.6, table 2.9, probes 1.2, records 0.2); the "
-                                 "walk is issue/latency-bound at ~3.0 TB/s average") if bsgs else
+                                 "(profiles/r01_bsgs_walk.txt) x d per step; algorithmic ~8.5 KB "
+                                 "per d (list 3.9, table 3.2, probes 1.1, records 0.3); the "
+                                 "window kernel is HBM-bound (per_kernel.window.hbm), the giant "
+                                 "kernel issue/latency-bound") if bsgs else
                                 "dram read+write bytes per walk launch, ncu --set full "
                                 "(profiles/r01_half_walk.txt); algorithmic bytes = 4 per d "
                                 "(survivor list) = 50.7 MB",

@@ -55,9 +55,9 @@ struct Ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // options
     int mode = EIS_MODE_AUTO;
-    u64 crossover = 1600000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
-                                     // HALF 1.02x faster at 1.4e9, BSGS 1.02x at 1.6e9,
-                                     // 1.19x at 3e9, 1.61x at 1e10, 2.8x at 1e11)
+    u64 crossover = 1450000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
+                                     // HALF 1.01x faster at 1.4e9, BSGS 1.02x at 1.5e9,
+                                     // 1.22x at 3e9, 1.65x at 1e10, 2.9x at 1e11)
     int alpha_x16 = 0;               // BSGS baby window W = alpha d^(1/4); 0 = by d (alpha_for)
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)

@@ -314,31 +314,6 @@ EIS_HD u32 win_step(WinLane &w) {
     return list_entry(f_to_u(w.st.Q), w.st.t2 >> 1);
 }
 
-// WIN_DEFER_EXIT: the lockstep loop only records in which step of an 8-step
-// block a symmetry exit fired (one bit per step); the result is derived after
-// the block from the entries (baby_result_f in terms of list entries: t of the
-// exit step k and of k - 1 and whether their Q agree, R13).  Capturing it per
-// step cost ~10 predicated instructions per step.
-#ifndef WIN_DEFER_EXIT
-#define WIN_DEFER_EXIT 0
-#endif
-EIS_HD u32 win_step_x(WinLane &w, bool &ex) {
-    ex = baby_step_fd(w.st, w.sqd_m, w.prod);
-    return list_entry(f_to_u(w.st.Q), w.st.t2 >> 1);
-}
-// exit at the first set bit k of exk; prev = the entry before e[0]
-EIS_HD void win_exit(WinLane &w, const u32 (&e)[8], u32 prev, u32 exk) {
-    const u32 k = (u32)__builtin_ctz_portable(exk);
-    u32 cur = e[0];
-#pragma unroll
-    for (int i = 1; i < 8; i++) {
-        if ((u32)i == k) { prev = e[i - 1]; cur = e[i]; }
-    }
-    const u32 tk = cur >> 20, tp = prev >> 20;
-    w.res = ((cur ^ prev) & 0xFFFFFu) == 0 ? tk + tp : 2u * tp;
-    w.live = false;
-}
-
 // fold the pending multipliers into the distance (every 4 steps: entry j = 3 mod 4)
 EIS_HD void win_flush(WinLane &w) {
     w.dist += log2_approx(w.prod);
@@ -701,7 +676,7 @@ __device__ __forceinline__ uint4 list_ld4(const uint4 *p) {
 // WIN_LD256: the build reads 8 entries per lane with one 32-byte load, which
 // also takes the evict_first priority as a plain qualifier (no createpolicy).
 #ifndef WIN_LD256
-#define WIN_LD256 0
+#define WIN_LD256 1
 #endif
 __device__ __forceinline__ void list_ld8(const u32 *p, uint4 &a, uint4 &b) {
     asm volatile("ld.global.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -877,26 +852,11 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         u32 *lst = o.lists + (u64)idx * B.lcap;
         if (w.live) baby += 7;                           // theta_2 (closed form) + 6
-#if WIN_DEFER_EXIT
-        {
-            u32 exk = 0;
-#pragma unroll
-            for (int k = 2; k < 8; k++) {
-                bool ex;
-                e[k] = win_step_x(w, ex);
-                exk |= (u32)ex << k;
-                if (k == 3 || k == 7) win_flush(w);
-            }
-            if (__any_sync(FULL_MASK, w.live && exk != 0))
-                if (w.live && exk != 0) win_exit(w, e, 0u, exk);
-        }
-#else
 #pragma unroll
         for (int k = 2; k < 8; k++) {
             e[k] = win_step(w);
             if (k == 3 || k == 7) win_flush(w);
         }
-#endif
         if (w.live) {
             store_block(lst, e);
             if (B.j1 == 7) win_mark_mu1(w);
@@ -904,25 +864,11 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         for (int blk = 1; blk < nblk; blk++) {
             if (!__any_sync(FULL_MASK, w.live)) break;
             if (w.live) baby += 8;
-#if WIN_DEFER_EXIT
-            const u32 elast = e[7];
-            u32 exk = 0;
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                bool ex;
-                e[k] = win_step_x(w, ex);
-                exk |= (u32)ex << k;
-                if (k == 3 || k == 7) win_flush(w);
-            }
-            if (__any_sync(FULL_MASK, w.live && exk != 0))
-                if (w.live && exk != 0) win_exit(w, e, elast, exk);
-#else
 #pragma unroll
             for (int k = 0; k < 8; k++) {
                 e[k] = win_step(w);
                 if (k == 3 || k == 7) win_flush(w);
             }
-#endif
             if (w.live) {
                 store_block(lst + blk * 8, e);
                 if (blk * 8 + 7 == B.j1) win_mark_mu1(w);

@@ -24,15 +24,15 @@ from . import count_buckets_dev, prefix_dev
 
 # Measured per-d device cost of the default (AUTO) path on one B200:
 # HALF below the crossover, rate ~ 2.68e8 (1e10/d)^(1/2) d/s; BSGS at and above
-# it, rate ~ 4.32e8 (1e10/d)^0.228 d/s.  Only the shape matters for splitting.
-AUTO_CROSSOVER = 1_600_000_000
+# it, rate ~ 4.42e8 (1e10/d)^0.228 d/s.  Only the shape matters for splitting.
+AUTO_CROSSOVER = 1_450_000_000
 
 
 def auto_cost_density(d: np.ndarray) -> np.ndarray:
     """Relative device time per candidate at d under EIS_MODE_AUTO."""
     d = np.maximum(np.asarray(d, dtype=np.float64), 1.0)
     half = (d / 1e10) ** 0.5 / 2.68e8
-    bsgs = (d / 1e10) ** 0.228 / 4.32e8
+    bsgs = (d / 1e10) ** 0.228 / 4.42e8
     return np.where(d < AUTO_CROSSOVER, half, bsgs)
 
 
@@ -43,7 +43,7 @@ def shard_bounds(lo: int, hi: int, world: int, rank: int, balance: str = "flat")
     fixed scale).  balance="prefix": equal cost for a prefix (0, X] where the
     per-d cost grows like d^(1/4), so the cumulative cost grows like x^(5/4):
     cut points x_g = X (g/G)^(4/5).  balance="auto": equal cost under the
-    measured cost of the AUTO path (HALF ~ d^(1/2) below 1.6e9, BSGS ~ d^0.228
+    measured cost of the AUTO path (HALF ~ d^(1/2) below 1.45e9, BSGS ~ d^0.228
     above), integrated numerically over (lo, hi].  Boundaries are rounded to
     multiples of 8 (never = 5 mod 8), so no candidate is split.
     """

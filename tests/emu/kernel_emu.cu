@@ -91,25 +91,13 @@ int main(int argc, char **argv) {
             if (!win_begin(w, d, e0, e1)) {
                 res = w.res;
             } else {                                        // window kernel, one lane
-                // the window kernel's 8-step blocks with deferred exit capture
-                u32 e[8];
-                e[0] = e0;
-                e[1] = e1;
-                for (int blk = 0; blk * 8 < B.nw && w.live; blk++) {
-                    const u32 elast = blk ? lst[blk * 8 - 1] : 0u;
-                    u32 exk = 0;
-                    for (int k = blk ? 0 : 2; k < 8; k++) {
-                        bool ex;
-                        e[k] = win_step_x(w, ex);
-                        exk |= (u32)ex << k;
-                        if ((k & 3) == 3) win_flush(w);
-                        baby++;
-                    }
-                    if (exk) win_exit(w, e, elast, exk);
-                    if (w.live) {
-                        for (int k = 0; k < 8; k++) lst[blk * 8 + k] = e[k];
-                        if (blk * 8 + 7 == B.j1) win_mark_mu1(w);
-                    }
+                lst[0] = e0;
+                lst[1] = e1;
+                for (int j = 2; j < B.nw && w.live; j++) {
+                    lst[j] = win_step(w);
+                    if ((j & 3) == 3) win_flush(w);
+                    baby++;
+                    if (j == B.j1 && w.live) win_mark_mu1(w);
                 }
                 if (!w.live) {
                     res = w.res;

@@ -105,7 +105,7 @@ def test_shard_bounds_properties():
 def test_auto_balance_equalises_model_cost():
     """balance="auto" (the distributed default): on the C5 prefix (0, 1e11] each
     of 8 shards carries 1/8 of the modelled AUTO-path device time (HALF below
-    the 1.6e9 crossover, BSGS above), to within the 8-aligned rounding."""
+    the 1.45e9 crossover, BSGS above), to within the 8-aligned rounding."""
     from paper_2507_06579_b200.dist import auto_cost_density
     X, G = 10**11, 8
     cuts = [shard_bounds(0, X, G, r, "auto") for r in range(G)]
