@@ -984,11 +984,14 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #define GIANT_MINB 7                          // 72 registers; with match_kind inlined 7 / 8 CTAs per SM measured 406.4 / 401.0 M d/s (8 spills more)
 #endif
 #ifndef PLAIN_TH
-// Alg. 4 l.742: the plain product for Q <= 50 (R6).  NUCOMP in exact fp64
-// cannot take its place: threshold 0 gave invariant violations at 5e10 (the
-// "can overflow" of l.733: w of a small-norm form is ~d/Q).  The coprime case
+// Alg. 4 l.742 takes the plain product for Q <= 50; the kernels take it for
+// Q <= 30 (R6).  NUCOMP in exact fp64 cannot take its place for small Q: w of a
+// small-norm form is ~d/Q (the "can overflow" of l.733).  Measured over the
+// full prefix to EIS_MAX_D = 1e11 (C5): threshold 20 gave 4.1 M invariant
+// violations (the call fails loudly), 30 none with byte-identical checkpoints;
+// 30 / 40 / 50 gave 450 / 448 / 446 M d/s on the bench slab.  The coprime case
 // of the plain product is a one-line CRT lift (forms.cuh plain_product).
-#define PLAIN_TH 50
+#define PLAIN_TH 30
 #endif
 #ifndef GIANT_DUP_FAST
 #define GIANT_DUP_FAST 0                      // 1: squarings in the giant kernel take nudupl_d
