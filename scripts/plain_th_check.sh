@@ -1,3 +1,5 @@
+# PLAIN_TH check: C5 (full prefix to 1e11) and pytest -m gpu on threshold variants, then an A/B at 1e10 and 1e11.
+# Expects build_variants/P20.so, P30.so (nvcc ... -DPLAIN_TH=N) and A_base.so, P40.so for the A/B.
 mkdir -p gpurun_out
 cp profiles/r01_c5_checkpoints.csv /tmp/c5_ref.csv
 for v in P20 P30; do
