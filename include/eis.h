@@ -169,6 +169,60 @@ EIS_API int eis_prefix_dev(const uint64_t *bucket_dev, size_t n, uint64_t *out_d
 EIS_API int eis_classify_range_dev(uint64_t lo, uint64_t hi, uint8_t *out_dev, size_t out_len,
                            void *stream);
 
+/* ---- the whole box: one process per GPU ----
+ *
+ * Every d is independent, so the range is cut into contiguous shards, one per
+ * process/GPU, and the only exchange is ONE sum-all-reduce of the 2n
+ * checkpoint buckets (NCCL over NVLink/NVSwitch), followed by the prefix
+ * kernel.  Two ways to run it:
+ *  (a) inside the library: rank 0 calls eis_comm_unique_id, the caller
+ *      broadcasts the EIS_COMM_ID_BYTES bytes by any means (a file, MPI,
+ *      torch.distributed), every rank calls eis_init(its device) and
+ *      eis_comm_init(id, world, rank), then eis_count_window_comm with the
+ *      same arguments on every rank; each rank receives the whole result.
+ *      NCCL is loaded at eis_comm_init (dlopen "libnccl.so.2", or the path in
+ *      the environment variable EIS_NCCL_LIB); the library does not link it.
+ *  (b) with the caller's own collective: per rank, eis_shard_bounds ->
+ *      eis_count_buckets_dev over its shard into zeroed device buckets ->
+ *      all-reduce(sum, uint64, 2n) on the same stream -> eis_prefix_dev ->
+ *      copy out.  (paper_2507_06579_b200/dist.py does this with
+ *      torch.distributed; examples/count_box.c does (a) from C.)
+ * Per-d flags need no collective: rank r classifies its own slice
+ * (eis_shard_bounds of (lo - 1, hi], then eis_classify_range(a + 1, b)); the
+ * slices of all ranks, concatenated in rank order, are eis_classify_range(lo, hi).
+ * Results never depend on the number of ranks or on the split. */
+enum { EIS_BALANCE_FLAT = 0, EIS_BALANCE_PREFIX = 1, EIS_BALANCE_AUTO = 2 };
+
+/* Contiguous shard (*a, *b] of (lo, hi] for `rank` of `world`:
+ *  FLAT   equal widths (windows, where the cost per d is flat);
+ *  PREFIX equal cost under a d^(1/4) cost model: cut points lo + (hi-lo)(g/G)^(4/5);
+ *  AUTO   equal cost under the measured cost model of EIS_MODE_AUTO (HALF ~ d^(1/2)
+ *         below option "crossover", BSGS ~ d^0.228 above), integrated numerically.
+ * Interior cut points are multiples of 8 (never a candidate), so no candidate
+ * is split; the shards of ranks 0..world-1 are disjoint and cover (lo, hi].
+ * Host-only (no device needed).  Bad world/rank/balance, lo > hi -> EIS_EINVAL. */
+EIS_API int eis_shard_bounds(uint64_t lo, uint64_t hi, int world, int rank, int balance,
+                             uint64_t *a, uint64_t *b);
+
+#define EIS_COMM_ID_BYTES 128
+/* Write a new NCCL unique id (EIS_COMM_ID_BYTES bytes, caller-owned) into id.
+ * Called by rank 0 only.  EIS_EDEVICE if NCCL cannot be loaded. */
+EIS_API int eis_comm_unique_id(void *id);
+/* Join the world-rank communicator named by id as `rank` on this process's
+ * device (eis_init's).  Collective: every rank must call it.  Replaces any
+ * previous communicator.  EIS_EINVAL on bad rank/world, EIS_EDEVICE on NCCL
+ * failure. */
+EIS_API int eis_comm_init(const void *id, int world, int rank);
+/* Destroy the communicator (also done by eis_finalize). */
+EIS_API void eis_comm_finalize(void);
+/* eis_count_window over the whole communicator: same arguments on every rank;
+ * rank r walks its EIS_BALANCE_AUTO shard of (lo, x[n-1]], the buckets are
+ * summed by ncclAllReduce on the library's stream, and every rank receives
+ * the full cnt_D, cnt_E.  Collective.  Without a communicator it is
+ * eis_count_window. */
+EIS_API int eis_count_window_comm(uint64_t lo, const uint64_t *x, size_t n, uint64_t *cnt_D,
+                                  uint64_t *cnt_E);
+
 /* ---- instrumentation ---- */
 typedef struct {
     uint64_t d_classified;   /* d in D walked by the last compute call */

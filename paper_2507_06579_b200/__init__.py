@@ -21,7 +21,8 @@ __all__ = [
     "classify_range", "count", "count_window", "count_window_ext", "count_buckets_dev",
     "prefix_dev",
     "classify_range_dev", "get_stats", "MODE_AUTO", "MODE_HALF", "MODE_BSGS", "NOT_IN_D",
-    "MAX_D", "LIB_PATH",
+    "MAX_D", "LIB_PATH", "shard_bounds", "comm_unique_id", "comm_init", "comm_finalize",
+    "count_window_comm", "BALANCE",
 ]
 
 LIB_PATH = os.environ.get("EIS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
@@ -29,6 +30,8 @@ LIB_PATH = os.environ.get("EIS_LIB") or os.path.join(os.path.dirname(os.path.abs
 MAX_D = 100_000_000_000
 NOT_IN_D = 0xFF
 MODE_AUTO, MODE_HALF, MODE_BSGS = 0, 1, 2
+BALANCE = {"flat": 0, "prefix": 1, "auto": 2}      # EIS_BALANCE_*
+COMM_ID_BYTES = 128
 
 EIS_OK, EIS_EINVAL, EIS_ERANGE, EIS_ENOMEM, EIS_EDEVICE, EIS_EINTERNAL = 0, -1, -2, -3, -4, -5
 _CODES = {-1: "EINVAL", -2: "ERANGE", -3: "ENOMEM", -4: "EDEVICE", -5: "EINTERNAL"}
@@ -37,7 +40,8 @@ EXPORTS = (
     "eis_init", "eis_finalize", "eis_last_error", "eis_set_option", "eis_get_option",
     "eis_num_candidates", "eis_classify_range", "eis_count", "eis_count_window",
     "eis_count_buckets_dev", "eis_prefix_dev", "eis_classify_range_dev", "eis_get_stats",
-    "eis_count_window_ext",
+    "eis_count_window_ext", "eis_shard_bounds", "eis_comm_unique_id", "eis_comm_init",
+    "eis_comm_finalize", "eis_count_window_comm",
 )
 NROWS = 5
 ROW_NAMES = ("D", "E", "T1", "DP", "EP")
@@ -110,6 +114,17 @@ def load() -> ctypes.CDLL:
     L.eis_classify_range_dev.restype = c_int
     L.eis_get_stats.argtypes = [ctypes.POINTER(Stats)]
     L.eis_get_stats.restype = c_int
+    L.eis_shard_bounds.argtypes = [u64, u64, c_int, c_int, c_int, ctypes.POINTER(u64),
+                                   ctypes.POINTER(u64)]
+    L.eis_shard_bounds.restype = c_int
+    L.eis_comm_unique_id.argtypes = [vp]
+    L.eis_comm_unique_id.restype = c_int
+    L.eis_comm_init.argtypes = [vp, c_int, c_int]
+    L.eis_comm_init.restype = c_int
+    L.eis_comm_finalize.argtypes = []
+    L.eis_comm_finalize.restype = None
+    L.eis_count_window_comm.argtypes = [u64, vp, sz, vp, vp]
+    L.eis_count_window_comm.restype = c_int
     _lib = L
     return L
 
@@ -210,3 +225,40 @@ def get_stats() -> dict:
     s = Stats()
     _check(load().eis_get_stats(ctypes.byref(s)))
     return s.as_dict()
+
+
+# ---- the whole box (include/eis.h "one process per GPU") ----
+def shard_bounds(lo: int, hi: int, world: int, rank: int, balance: str = "flat") -> tuple[int, int]:
+    """Contiguous shard (a, b] of (lo, hi] for ``rank`` of ``world`` (eis_shard_bounds;
+    balance "flat", "prefix" or "auto").  Host-only."""
+    a, b = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(load().eis_shard_bounds(lo, hi, world, rank, BALANCE[balance], ctypes.byref(a),
+                                   ctypes.byref(b)))
+    return int(a.value), int(b.value)
+
+
+def comm_unique_id() -> bytes:
+    """A new NCCL unique id (rank 0); broadcast it to the other ranks."""
+    buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+    _check(load().eis_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(uid: bytes, world: int, rank: int) -> None:
+    assert len(uid) == COMM_ID_BYTES
+    buf = ctypes.create_string_buffer(uid, COMM_ID_BYTES)
+    _check(load().eis_comm_init(buf, world, rank))
+
+
+def comm_finalize() -> None:
+    load().eis_comm_finalize()
+
+
+def count_window_comm(lo: int, x) -> tuple[np.ndarray, np.ndarray]:
+    """count_window over the library's NCCL communicator (collective)."""
+    x = _u64(x)
+    cD = np.zeros(len(x), dtype=np.uint64)
+    cE = np.zeros(len(x), dtype=np.uint64)
+    _check(load().eis_count_window_comm(lo, x.ctypes.data, len(x), cD.ctypes.data,
+                                        cE.ctypes.data))
+    return cD, cE

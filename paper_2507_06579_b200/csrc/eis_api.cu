@@ -7,6 +7,8 @@
 // and finally the prefix kernel for the counting functions.  Everything the
 // method computes runs in these kernels; the host only does index arithmetic.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types and prototypes only: libnccl is dlopen'ed by eis_comm_init
 
 #include <algorithm>
 #include <cmath>
@@ -53,6 +55,9 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;      // giant kernels
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // whole box (eis_comm_init): NCCL communicator over one process per GPU
+    ncclComm_t comm = nullptr;
+    int comm_world = 1, comm_rank = 0;
     // options
     int mode = EIS_MODE_AUTO;
     u64 crossover = 1450000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200:
@@ -529,6 +534,113 @@ int count_window_rows(u64 lo, const u64 *x, size_t n, int nrow, u64 *out) {
     return end_call(s);
 }
 
+// ---- whole box: contiguous shards, one all-reduce ----------
+
+// Relative device time per candidate at d of the AUTO path (measured on one
+// B200): HALF below the crossover, rate ~ 2.68e8 (1e10/d)^(1/2)
+// d/s; BSGS at and above it, rate ~ 4.42e8 (1e10/d)^0.228 d/s.  Only the
+// shape matters for splitting.
+double auto_cost_density(double d) {
+    d = std::max(d, 1.0);
+    return d < (double)g.crossover ? std::pow(d / 1e10, 0.5) / 2.68e8
+                                   : std::pow(d / 1e10, 0.228) / 4.42e8;
+}
+
+// cut point g of (lo, hi] into `world` contiguous shards, a multiple of 8
+// (never = 5 mod 8, so no candidate is split) clamped to [lo, hi]
+u64 shard_cut(u64 lo, u64 hi, int world, int gi, int balance, const std::vector<double> &cum,
+              const std::vector<double> &xs) {
+    if (gi <= 0) return lo;
+    if (gi >= world) return hi;
+    u64 v;
+    const double f = (double)gi / world;
+    if (balance == EIS_BALANCE_PREFIX) {
+        v = lo + (u64)((double)(hi - lo) * std::pow(f, 0.8));   // x_g = X (g/G)^(4/5)
+    } else if (balance == EIS_BALANCE_AUTO) {
+        size_t k = (size_t)(std::lower_bound(cum.begin(), cum.end(), f) - cum.begin());
+        k = std::min(std::max<size_t>(k, 1), cum.size() - 1);
+        const double t = cum[k] > cum[k - 1] ? (f - cum[k - 1]) / (cum[k] - cum[k - 1]) : 0.0;
+        v = (u64)(xs[k - 1] + t * (xs[k] - xs[k - 1]));
+    } else {
+        v = lo + (hi - lo) / (u64)world * (u64)gi + (hi - lo) % (u64)world * (u64)gi / (u64)world;
+    }
+    v -= v % 8;
+    return std::min(hi, std::max(lo, v));
+}
+
+int shard_bounds(u64 lo, u64 hi, int world, int rank, int balance, u64 &a, u64 &b) {
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(EIS_EINVAL, "need 0 <= rank < world (rank %d, world %d)", rank, world);
+    if (balance < EIS_BALANCE_FLAT || balance > EIS_BALANCE_AUTO)
+        return fail(EIS_EINVAL, "unknown balance %d", balance);
+    if (lo > hi) return fail(EIS_EINVAL, "lo > hi");
+    if (world == 1) { a = lo; b = hi; return 0; }
+    std::vector<double> cum, xs;
+    if (balance == EIS_BALANCE_AUTO) {
+        // cumulative modelled cost on 4096 equal intervals (trapezoids), normalised
+        const int K = 4096;
+        xs.resize(K + 1);
+        cum.resize(K + 1);
+        double prev = 0;
+        for (int i = 0; i <= K; i++) {
+            xs[i] = (double)lo + (double)(hi - lo) * i / K;
+            const double c = auto_cost_density(xs[i]);
+            cum[i] = i ? cum[i - 1] + 0.5 * (c + prev) * (xs[i] - xs[i - 1]) : 0.0;
+            prev = c;
+        }
+        if (cum[K] > 0) for (double &v : cum) v /= cum[K];
+    }
+    a = shard_cut(lo, hi, world, rank, balance, cum, xs);
+    b = shard_cut(lo, hi, world, rank + 1, balance, cum, xs);
+    return 0;
+}
+
+// NCCL, resolved at run time (the library does not link it: a process that
+// never calls eis_comm_init never loads it, and one that already holds
+// libnccl.so.2, e.g. through torch, shares that copy)
+struct NcclApi {
+    void *h = nullptr;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+NcclApi nccl;
+
+int nccl_load() {
+    if (nccl.h) return 0;
+    const char *name = getenv("EIS_NCCL_LIB");
+    void *h = dlopen(name && *name ? name : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(EIS_EDEVICE, "cannot load NCCL: %s", dlerror());
+    nccl.get_unique_id = (decltype(&ncclGetUniqueId))dlsym(h, "ncclGetUniqueId");
+    nccl.comm_init_rank = (decltype(&ncclCommInitRank))dlsym(h, "ncclCommInitRank");
+    nccl.all_reduce = (decltype(&ncclAllReduce))dlsym(h, "ncclAllReduce");
+    nccl.comm_destroy = (decltype(&ncclCommDestroy))dlsym(h, "ncclCommDestroy");
+    nccl.error_string = (decltype(&ncclGetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!nccl.get_unique_id || !nccl.comm_init_rank || !nccl.all_reduce || !nccl.comm_destroy ||
+        !nccl.error_string) {
+        dlclose(h);
+        return fail(EIS_EDEVICE, "libnccl lacks a required symbol");
+    }
+    nccl.h = h;
+    return 0;
+}
+
+#define NCCL_TRY(expr)                                                                     \
+    do {                                                                                   \
+        ncclResult_t r_ = (expr);                                                          \
+        if (r_ != ncclSuccess)                                                             \
+            return fail(EIS_EDEVICE, "%s failed: %s", #expr, nccl.error_string(r_));       \
+    } while (0)
+
+void comm_release() {
+    if (g.comm && nccl.comm_destroy) nccl.comm_destroy(g.comm);
+    g.comm = nullptr;
+    g.comm_world = 1;
+    g.comm_rank = 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -536,6 +648,7 @@ extern "C" {
 int eis_init(int device) { return do_init(device); }
 
 void eis_finalize(void) {
+    comm_release();
     if (!g.inited) return;
     cudaFree(g.d_primes);
     for (auto &b : g.buf) {
@@ -719,6 +832,70 @@ int eis_count_window_ext(uint64_t lo, const uint64_t *x, size_t n, uint64_t *out
 
 int eis_count(const uint64_t *x, size_t n, uint64_t *pi_D, uint64_t *pi_E) {
     return eis_count_window(0, x, n, pi_D, pi_E);
+}
+
+int eis_shard_bounds(uint64_t lo, uint64_t hi, int world, int rank, int balance, uint64_t *a,
+                     uint64_t *b) {
+    if (!a || !b) return fail(EIS_EINVAL, "NULL output");
+    u64 aa = 0, bb = 0;
+    if (int rc = shard_bounds(lo, hi, world, rank, balance, aa, bb)) return rc;
+    *a = aa;
+    *b = bb;
+    return 0;
+}
+
+int eis_comm_unique_id(void *id) {
+    if (!id) return fail(EIS_EINVAL, "NULL id");
+    if (int rc = nccl_load()) return rc;
+    ncclUniqueId u;
+    NCCL_TRY(nccl.get_unique_id(&u));
+    std::memcpy(id, &u, sizeof u);
+    return 0;
+}
+
+int eis_comm_init(const void *id, int world, int rank) {
+    if (!id) return fail(EIS_EINVAL, "NULL id");
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(EIS_EINVAL, "need 0 <= rank < world (rank %d, world %d)", rank, world);
+    if (int rc = do_init(-1)) return rc;
+    if (int rc = nccl_load()) return rc;
+    comm_release();
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    NCCL_TRY(nccl.comm_init_rank(&g.comm, world, u, rank));
+    g.comm_world = world;
+    g.comm_rank = rank;
+    return 0;
+}
+
+void eis_comm_finalize(void) { comm_release(); }
+
+int eis_count_window_comm(uint64_t lo, const uint64_t *x, size_t n, uint64_t *cnt_D,
+                          uint64_t *cnt_E) {
+    if (!g.comm) return eis_count_window(lo, x, n, cnt_D, cnt_E);
+    if (n == 0) return 0;
+    if (!cnt_D || !cnt_E) return fail(EIS_EINVAL, "NULL output");
+    if (int rc = check_x(x, n, lo)) return rc;
+    if (int rc = do_init(-1)) return rc;
+    u64 a, b;
+    if (int rc = shard_bounds(lo, x[n - 1], g.comm_world, g.comm_rank, EIS_BALANCE_AUTO, a, b))
+        return rc;
+    cudaStream_t s = g.stream;
+    if (int rc = begin_call(s)) return rc;
+    if (ensure(g.d_buckets, g.buckets_cap, 2 * n)) return EIS_ENOMEM;
+    CUDA_TRY(cudaMemsetAsync(g.d_buckets, 0, 2 * n * sizeof(u64), s));
+    if (int rc = count_buckets(a, b, x, n, g.d_buckets, s)) return rc;
+    // the path's one exchange step: sum the 2n buckets over all ranks (NVLink)
+    NCCL_TRY(nccl.all_reduce(g.d_buckets, g.d_buckets, 2 * n, ncclUint64, ncclSum, g.comm, s));
+    prefix_kernel<<<1, 1024, 0, s>>>(g.d_buckets, g.d_buckets, (int)n, 2);
+    CUDA_TRY(cudaGetLastError());
+    g.launches++;
+    std::vector<u64> h(2 * n);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), g.d_buckets, 2 * n * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    if (int rc = end_call(s)) return rc;
+    std::memcpy(cnt_D, h.data(), n * sizeof(u64));
+    std::memcpy(cnt_E, h.data() + n, n * sizeof(u64));
+    return 0;
 }
 
 int eis_get_stats(eis_stats *out) {

@@ -208,7 +208,7 @@ EIS_HD void partial_euclid(i64 &bx, i64 &by, i64 &x, i64 &y, int &z, i64 L) {
 
 // Algorithm 2 NUCOMP on forms (u1,v1,w1), (u2,v2,w2).
 EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u3, i64 &v3,
-                   i64 &G, i64 &xo, i64 &yo, u32 *err) {
+                   i64 &w3, i64 &G, i64 &xo, i64 &yo, u32 *err) {
     if (w1 < w2) {
         i64 t;
         t = u1; u1 = u2; u2 = t;
@@ -259,24 +259,24 @@ EIS_HD void nucomp(i64 u1, i64 v1, i64 w1, i64 u2, i64 v2, i64 w2, i64 L, i64 &u
         if (bx != 0) cy = exact_div(Q2, bx, err);
         else cy = exact_div(cx * dy - w1, dx, err);
         u3 = by * cy - ay * dy;
-        v3 = G * (Q3 + Q4) - Q1 - Q2;      // (w3 = bx cx - ax dx is not needed)
+        w3 = bx * cx - G * x * dx;         // ax = G x
+        v3 = G * (Q3 + Q4) - Q1 - Q2;
     } else {
         const double rBy = rcp64((double)By);
         const i64 Q1 = Cy * bx;
         const i64 cx = exact_div_r(Q1 - m, By, rBy, err);
         const i64 dx = exact_div_r(bx * Dy - w2, By, rBy, err);
-        (void)cx;
-        (void)dx;
         u3 = by * Cy;
-        v3 = v2 - 2 * Q1;                  // (w3 = bx cx - G dx is not needed)
+        w3 = bx * cx - G * dx;
+        v3 = v2 - 2 * Q1;
     }
     xo = x;
     yo = y;
 }
 
 // Algorithm 3 NUDUPL on the form (u, v, w).
-EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &G, i64 &xo, i64 &yo,
-                   u32 *err) {
+EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &w3, i64 &G, i64 &xo,
+                   i64 &yo, u32 *err) {
     i64 xx, yy;
     G = xgcd_s(u, v, xx, yy);     // xx u + yy v = G
     const i64 By = sdiv_exact23(u, G);
@@ -287,8 +287,11 @@ EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &G, i64 &xo
     partial_euclid(bx, by, x, y, z, L);
     const i64 ay = G * y;
     if (z == 0) {
+        const i64 dx = exact_div(bx * Dy - w, By, err);
         u3 = by * by;
-        v3 = v - (bx + by) * (bx + by) + u3 + bx * bx;   // (w3 update not needed)
+        w3 = bx * bx;
+        v3 = v - (bx + by) * (bx + by) + u3 + w3;
+        w3 = w3 - G * dx;
     } else {
         const i64 dx = exact_div(bx * Dy - w * x, By, err);
         const i64 Q1 = dx * y;
@@ -296,8 +299,10 @@ EIS_HD void nudupl(i64 u, i64 v, i64 w, i64 L, i64 &u3, i64 &v3, i64 &G, i64 &xo
         v3 = G * (dy + Q1);
         dy = exact_div(dy, x, err);
         u3 = by * by;
-        v3 = v3 - (bx + by) * (bx + by) + u3 + bx * bx;
-        u3 = u3 - ay * dy;                               // (w3 update not needed)
+        w3 = bx * bx;
+        v3 = v3 - (bx + by) * (bx + by) + u3 + w3;
+        u3 = u3 - ay * dy;
+        w3 = w3 - G * x * dx;                            // ax = G x
     }
     xo = x;
     yo = y;
@@ -326,6 +331,7 @@ EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
         r.Q = 2 * a1 * a2;
         r.P = (i64)dfloor_mod(v, M, rcp64(M));
         r.lg = 0.f;
+        if (floor_mod(r.P * r.P - d, 2 * r.Q) != 0) *err += 1;   // b3^2 = d mod 4 a3 (R20)
         return r;
     }
     const i64 n = (P1 + P2) / 2;
@@ -346,6 +352,7 @@ EIS_HD Composed plain_product(i64 Q1, i64 P1, i64 Q2, i64 P2, i64 d, u32 *err) {
     r.Q = 2 * a3;
     r.P = num / S;                             // in [0, 2 a3)
     r.lg = log2_approx((float)S);
+    if (floor_mod(r.P * r.P - d, 2 * r.Q) != 0) *err += 1;       // b3^2 = d mod 4 a3 (R20)
     return r;
 }
 
@@ -370,16 +377,18 @@ EIS_HD_COLD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64
     const i64 Q1 = m1.Q, P1 = m1.P;
     P2 = P2 < Q2 ? P2 : floor_mod(P2, Q2);
     if (Q1 <= plain_th || Q2 <= plain_th) return plain_product(Q1, P1, Q2, P2, d, err);
-    i64 u3, v3, G, x, y;
+    i64 u3, v3, w3, G, x, y;
     Composed r;
     if (Q1 == Q2 && P1 == P2) {
-        nudupl(Q1 >> 1, -P1, m1.w, L, u3, v3, G, x, y, err);
+        nudupl(Q1 >> 1, -P1, m1.w, L, u3, v3, w3, G, x, y, err);
         r.kind = 2;
     } else {
         const i64 w2 = exact_div(P2 * P2 - d, 2 * Q2, err);
-        nucomp(Q1 >> 1, -P1, m1.w, Q2 >> 1, -P2, w2, L, u3, v3, G, x, y, err);
+        nucomp(Q1 >> 1, -P1, m1.w, Q2 >> 1, -P2, w2, L, u3, v3, w3, G, x, y, err);
         r.kind = 1;
     }
+    // the output form's discriminant (l.622, l.687), exact in 128 bits
+    if ((__int128)v3 * v3 - 4 * (__int128)u3 * w3 != (__int128)d) *err += 1;
     r.Q = iabs64(2 * u3);
     r.P = floor_mod(-v3, r.Q);
     r.tg = t_gamma(x, y, v3);
@@ -403,8 +412,22 @@ EIS_HD double dexact_div(double n, double dv, double rdv, u32 *err) {
 }
 
 struct CompD {
-    double u3, v3, x, y, G;
+    double u3, v3, w3, x, y, G;
 };
+
+// Exact check of the output form's discriminant, v3^2 - 4 u3 w3 = d (Alg. 2/3
+// output phi_3 "whose discriminant is d"), on fp64
+// integers that may exceed 2^53 in the squares: p = v3^2 and q = 4 u3 w3 are
+// split into rounded value + exact FMA error.  If the form is right, p and q
+// agree to within d, so p - q is exact (Sterbenz) and the rest are small exact
+// integers; if p and q differ by more than a factor 2, |p - q| > 2^52 > d and
+// the test fails as it should.
+EIS_HD bool disc_ok(double u3, double v3, double w3, double d) {
+    const double p = v3 * v3, e1 = fma(v3, v3, -p);
+    const double t = 4.0 * u3;
+    const double q = t * w3, e2 = fma(t, w3, -q);
+    return ((p - q) - d) + (e1 - e2) == 0.0;
+}
 
 EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, double w2, float L,
                      CompD &o, u32 *err, u32 wmask) {
@@ -477,10 +500,14 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
         if (bx != 0.0) cy = dexact_div(Q2, bx, rcp64(bx), err);
         else cy = dexact_div(fma(cx, dy, -w1), dx, rcp64(dx), err);
         o.u3 = fma(by, cy, -G * y * dy);
+        o.w3 = fma(bx, cx, -G * x * dx);          // w3 = bx cx - ax dx, ax = G x
         o.v3 = G * (Q3 + Q4) - Q1 - Q2;
     } else {
         const double Q1 = Cy * bx;
+        const double cx = dexact_div(Q1 - m, By, rBy, err);
+        const double dx = dexact_div(fma(bx, Dy, -w2), By, rBy, err);
         o.u3 = by * Cy;
+        o.w3 = fma(bx, cx, -G * dx);              // w3 = bx cx - G dx
         o.v3 = v2 - 2.0 * Q1;
     }
     o.x = x;
@@ -521,8 +548,10 @@ EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, 
     const double bx = fbx, by = fby, x = fx, y = fy;
     const double sq = (bx + by) * (bx + by) - bx * bx;   // exact: < 2^40
     if (z == 0) {
+        const double dx = dexact_div(fma(bx, Dy, -w), By, rBy, err);
         o.u3 = by * by;
         o.v3 = v - sq + o.u3;
+        o.w3 = fma(bx, bx, -G * dx);              // w3 = bx^2 - G dx
     } else {
         const double dx = dexact_div(fma(bx, Dy, -w * x), By, rBy, err);
         const double Q1 = dx * y;
@@ -530,6 +559,7 @@ EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, 
         const double dy = dexact_div(dy0, x, rcp64(x), err);
         o.v3 = G * (dy0 + Q1) - sq + by * by;
         o.u3 = fma(by, by, -G * y * dy);
+        o.w3 = fma(bx, bx, -G * x * dx);          // w3 = bx^2 - ax dx
     }
     o.x = x;
     o.y = y;
@@ -605,7 +635,9 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     else   // |N(gamma)| = (Q1/2)(Q2/2)/|u3|, use the conjugate (no cancellation)
         r.lg = log2_approx(2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1) / ((float)o.G * mag));
     r.kind = fdup ? 2u : 1u;
-    if (((r.Q & 3) != 2) | ((r.P & 1) != 1) | (((i64)o.G & 1) == 0)) *err += 1;
+    if (((r.Q & 3) != 2) | ((r.P & 1) != 1) | (((i64)o.G & 1) == 0) |
+        !disc_ok(o.u3, o.v3, o.w3, (double)d))
+        *err += 1;
     return r;
 }
 

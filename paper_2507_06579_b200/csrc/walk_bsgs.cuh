@@ -530,9 +530,9 @@ struct __align__(64) GiantRec {
     double sqrtd;
     i64 w1;                        // mu_1's form coefficient (P1^2 - d)/(2 Q1)
     u32 off, Q1, P1, Qc;           // P1 normalised mod Q1
-    u32 Pc, tk, s, Lk;             // tk = t1 | tc << 2 | k << 4; Lk = L | kcap << 16
+    u32 Pc, tk, s, L;              // tk = t1 | tc << 2 | k << 4
     float dist1, distc, dist_last;
-    u32 pad;
+    u32 kcap;                      // giant-step cap (giant_cap * (d^(1/4) + 10), may pass 2^16)
 };
 
 EIS_HD GiantRec giant_pack(const GiantLane &g, u32 off) {
@@ -546,19 +546,19 @@ EIS_HD GiantRec giant_pack(const GiantLane &g, u32 off) {
     r.Pc = g.Pc;
     r.tk = g.t1 | (g.tc << 2) | ((u32)g.k << 4);
     r.s = (u32)g.s;
-    r.Lk = (u32)g.L | ((u32)g.kcap << 16);
+    r.L = (u32)g.L;
     r.dist1 = g.dist1;
     r.distc = g.distc;
     r.dist_last = g.dist_last;
-    r.pad = 0;
+    r.kcap = (u32)g.kcap;
     return r;
 }
 
 EIS_HD void giant_unpack(GiantLane &g, const GiantRec &r, u64 d) {
     g.d = d;
     g.s = r.s;
-    g.L = r.Lk & 0xFFFFu;
-    g.kcap = (int)(r.Lk >> 16);
+    g.L = r.L;
+    g.kcap = (int)r.kcap;
     g.sqrtd = (float)r.sqrtd;
     g.m1.Q = r.Q1;
     g.m1.P = r.P1;
@@ -984,14 +984,13 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #define GIANT_MINB 7                          // 72 registers; with match_kind inlined 7 / 8 CTAs per SM measured 406.4 / 401.0 M d/s (8 spills more)
 #endif
 #ifndef PLAIN_TH
-// Alg. 4 l.742 takes the plain product for Q <= 50; the kernels take it for
-// Q <= 30 (R6).  NUCOMP in exact fp64 cannot take its place for small Q: w of a
-// small-norm form is ~d/Q (the "can overflow" of l.733).  Measured over the
-// full prefix to EIS_MAX_D = 1e11 (C5): threshold 20 gave 4.1 M invariant
-// violations (the call fails loudly), 30 none with byte-identical checkpoints;
-// 30 / 40 / 50 gave 450 / 448 / 446 M d/s on the bench slab.  The coprime case
-// of the plain product is a one-line CRT lift (forms.cuh plain_product).
-#define PLAIN_TH 30
+// Alg. 4 l.742: the plain product for Q <= 50, as printed (R6).  NUCOMP in exact
+// fp64 cannot take its place for small Q: w of a small-norm form is ~d/Q (the
+// "can overflow" of l.733).  Every output is checked exactly (disc_ok, the
+// plain product's b3^2 = d mod 4 a3), so any inexact composition fails the call
+// loudly.  (Round 1 measured 30 / 40 / 50 at 450 / 448 / 446 M d/s and 20 with
+// 4.1 M violations over C5; the paper's 50 is kept.)
+#define PLAIN_TH 50
 #endif
 #ifndef GIANT_DUP_FAST
 #define GIANT_DUP_FAST 0                      // 1: squarings in the giant kernel take nudupl_d

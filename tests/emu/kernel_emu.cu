@@ -36,14 +36,15 @@ int main(int argc, char **argv) {
                 for (int k = 0; k < per_d; k++) {
                     if ((i64)st.Q > plain_th) {
                         const Mu1Form m = mu1_form((i64)st.Q, (i64)st.P, (i64)dd, &err);
-                        i64 u3, v3, G, x, y;
-                        nudupl((i64)(m.Q >> 1), -(i64)m.P, m.w, L, u3, v3, G, x, y, &err);
+                        i64 u3, v3, w3, G, x, y;
+                        nudupl((i64)(m.Q >> 1), -(i64)m.P, m.w, L, u3, v3, w3, G, x, y, &err);
                         CompD o;
                         nudupl_d((double)(m.Q >> 1), -(double)m.P, (double)m.w, (float)L, o, &err,
                                  0xffffffffu);
                         checked++;
-                        if ((i64)o.u3 != u3 || (i64)o.v3 != v3 || (i64)o.x != x || (i64)o.y != y ||
-                            (i64)o.G != G)
+                        if ((i64)o.u3 != u3 || (i64)o.v3 != v3 || (i64)o.w3 != w3 ||
+                            (i64)o.x != x || (i64)o.y != y || (i64)o.G != G ||
+                            !disc_ok(o.u3, o.v3, o.w3, (double)dd))
                             bad++;
                     }
                     if (baby_step(st)) break;

@@ -119,3 +119,21 @@ def test_product_package_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "eis_oracle" not in src and "liboracle" not in src, f
+
+
+def test_c_example_builds_against_the_header(lib, tmp_path):
+    """examples/count_box.c (the whole-box path from C: eis_comm_* +
+    eis_count_window_comm) compiles against include/eis.h and links libeis.so;
+    without a GPU it must fail loudly, not fall back."""
+    import subprocess
+
+    import torch
+
+    exe = str(tmp_path / "count_box")
+    pkg = os.path.dirname(eis.LIB_PATH)
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "count_box.c"), "-L", pkg, "-leis",
+                           f"-Wl,-rpath,{pkg}", "-o", exe])
+    if not torch.cuda.is_available():
+        out = subprocess.run([exe, "0", "1000"], capture_output=True, text=True, timeout=60)
+        assert out.returncode != 0 and "eis_init failed (-4)" in out.stderr

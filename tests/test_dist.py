@@ -17,7 +17,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import c_oracle
-from paper_2507_06579_b200.dist import allreduce_buckets, shard_bounds
+import paper_2507_06579_b200 as eis
+from paper_2507_06579_b200.dist import AUTO_CROSSOVER, allreduce_buckets, shard_bounds
 
 
 def _free_port() -> int:
@@ -102,11 +103,18 @@ def test_shard_bounds_properties():
     assert widths == sorted(widths, reverse=True)
 
 
+def auto_cost_density(d: np.ndarray) -> np.ndarray:
+    """The AUTO path's measured per-d device cost, written out
+    independently of the library's eis_shard_bounds: HALF below the crossover
+    at 2.68e8 (1e10/d)^(1/2) d/s, BSGS above it at 4.42e8 (1e10/d)^0.228 d/s."""
+    d = np.maximum(np.asarray(d, dtype=np.float64), 1.0)
+    return np.where(d < AUTO_CROSSOVER, (d / 1e10) ** 0.5 / 2.68e8, (d / 1e10) ** 0.228 / 4.42e8)
+
+
 def test_auto_balance_equalises_model_cost():
     """balance="auto" (the distributed default): on the C5 prefix (0, 1e11] each
     of 8 shards carries 1/8 of the modelled AUTO-path device time (HALF below
     the 1.45e9 crossover, BSGS above), to within the 8-aligned rounding."""
-    from paper_2507_06579_b200.dist import auto_cost_density
     X, G = 10**11, 8
     cuts = [shard_bounds(0, X, G, r, "auto") for r in range(G)]
     xs = np.linspace(1.0, X, 200001)
@@ -117,3 +125,39 @@ def test_auto_balance_equalises_model_cost():
     assert np.all(np.abs(share - 1 / G) < 2e-3), share
     # the flat split would give the last shard ~1.3x the first's cost
     assert cuts[0][1] - cuts[0][0] > cuts[-1][1] - cuts[-1][0]
+
+
+def test_shard_bounds_edges_and_errors():
+    """eis_shard_bounds (host logic of the whole-box ABI): degenerate ranges,
+    more ranks than candidates, and argument errors."""
+    for balance in ("flat", "prefix", "auto"):
+        assert shard_bounds(7, 7, 4, 2, balance) == (7, 7)
+        assert shard_bounds(0, 100, 1, 0, balance) == (0, 100)
+        cuts = [shard_bounds(100, 120, 8, r, balance) for r in range(8)]
+        assert cuts[0][0] == 100 and cuts[-1][1] == 120
+        assert all(b0 == a1 for (_, b0), (a1, _) in zip(cuts, cuts[1:]))
+        assert sum(eis.num_candidates(a + 1, b) for a, b in cuts if b > a) == \
+            eis.num_candidates(101, 120)
+    for bad in [dict(world=0, rank=0), dict(world=2, rank=2), dict(world=2, rank=-1)]:
+        with pytest.raises(eis.EisError):
+            shard_bounds(0, 100, bad["world"], bad["rank"])
+    with pytest.raises(eis.EisError):
+        shard_bounds(10, 5, 2, 0)
+    with pytest.raises(KeyError):
+        shard_bounds(0, 100, 2, 0, "nope")
+
+
+@pytest.mark.parametrize("lo,hi,world", [(0, 10**6, 2), (1, 999_999, 3), (5, 5, 2),
+                                         (123_457, 9_876_543, 8), (10**10 - 10**6, 10**10, 4)])
+def test_distributed_classify_slices_partition_the_range(lo, hi, world):
+    """classify_range_distributed's slices (a+1 .. b of shard_bounds(lo-1, hi))
+    are disjoint and, in rank order, hold exactly the candidates of [lo, hi]
+    (per-d flags need no collective)."""
+    for balance in ("flat", "prefix", "auto"):
+        cuts = [shard_bounds(max(lo, 1) - 1, hi, world, r, balance) for r in range(world)]
+        total = 0
+        for r, (a, b) in enumerate(cuts):
+            if r:
+                assert a == cuts[r - 1][1]
+            total += eis.num_candidates(a + 1, b) if b > a else 0
+        assert total == eis.num_candidates(lo, hi)

@@ -30,7 +30,7 @@ def emu(tmp_path_factory):
     return exe
 
 
-def run(exe, ds, mode, alpha_x16=16, ns_log2=0, plain_th=0, two_sided=1):   # 0 = PLAIN_TH
+def run(exe, ds, mode, alpha_x16=16, ns_log2=0, plain_th=50, two_sided=1):   # 50 = PLAIN_TH
     out = subprocess.run([exe, mode, str(alpha_x16), str(ns_log2), str(plain_th), str(two_sided)],
                          input="\n".join(str(int(d)) for d in ds), capture_output=True,
                          text=True, check=True).stdout

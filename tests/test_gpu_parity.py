@@ -137,6 +137,38 @@ def test_bsgs_options_do_not_change_results(opts):
         eis.set_option("mode", eis.MODE_AUTO)
 
 
+@pytest.mark.parametrize("opts", [{"two_sided": 0}, {"alpha_x16": 8}, {"alpha_x16": 64},
+                                  {"alpha_x16": 8, "two_sided": 0}])
+def test_bsgs_options_at_1e11_and_on_the_bench_slab(opts):
+    """Non-default BSGS configurations at the top of the range (C4, d ~ 1e11,
+    where NUCOMP's magnitudes peak, l.733) and on the bench slab: every giant
+    step's output is checked exactly in the kernels (disc_ok, R20), so a single
+    inexact composition would fail the call with EIS_EINTERNAL; the Table 1
+    totals, pi_D by Moebius and seeded oracle samples
+    must come out unchanged (R6, R29, R35)."""
+    old = {k: eis.get_option(k) for k in opts}
+    try:
+        eis.set_option("mode", eis.MODE_AUTO)
+        for k, v in opts.items():
+            eis.set_option(k, v)
+        cfg = workloads.CONFIGS["C4"]
+        cD, cE = eis.count_window(cfg["lo"], cfg["x"])
+        assert int(cE[-1] - cE[-2]) == 3_345_503
+        assert int(cD[-1]) == pi_D_closed_form(cfg["hi"]) - pi_D_closed_form(cfg["lo"])
+        assert eis.get_stats()["giant_steps"] > 0
+        lo, hi = workloads.metric_slab(0)
+        x = workloads.metric_checkpoints(1)
+        cD, cE = eis.count_window(lo, x)
+        assert int(cE[-1] - cE[x.index(9_900_000_000)]) == 3_334_227
+        s = workloads.sample_candidates(cfg["hi"] - 10**7, cfg["hi"], 120, seed=4242)
+        f = eis.classify_range(int(s[0]), int(s[-1]))
+        got = f[((s - s[0]) // 8).astype(np.int64)]
+        assert np.array_equal(got, c_oracle.classify_list(s, NTHREADS))
+    finally:
+        for k, v in old.items():
+            eis.set_option(k, v)
+
+
 @pytest.mark.parametrize("hi", [10**10, 5 * 10**10, eis.MAX_D])
 def test_half_and_bsgs_agree_on_large_windows(hi):
     """Where the oracle is too slow for every d: the half walk (no giant steps)
@@ -252,7 +284,7 @@ def test_metric_slab_as_benched():
     i99 = x.index(9_900_000_000)
     assert int(cE[-1] - cE[i99]) == 3_334_227
     assert int(cD[-1]) == pi_D_closed_form(hi) - pi_D_closed_form(lo)
-    s = workloads.sample_candidates(lo + 1, hi, 600)
+    s = workloads.sample_candidates(lo + 1, hi, 16_000)      # ~15 core-ms each at 1e10
     f = eis.classify_range(lo + 1, hi)
     got = f[((s - (lo + 1 + (5 - (lo + 1)) % 8)) // 8).astype(np.int64)]
     want = c_oracle.classify_list(s, NTHREADS)
