@@ -34,27 +34,27 @@ import workloads  # noqa: E402
 METRIC = "squarefree d≡5 mod 8 classified/sec (whole box) at d≈10^10; 1/2/4/8 B200"
 UNIT = "d/s"
 SM_MAX_MHZ_FALLBACK = 1965.0
-# Algorithmic thread-operations per unit of work:
-# Work per unit: one rho step (+ residue + exit tests) is 14 SASS
-# instructions in the kernel's FP32 formulation (cuobjdump), so `frac` is the
-# share of the chip's issue slots spent on step instructions.  SURVEY 8(d)'s
-# generic u32 step is 34 instructions; `work_equiv_generic` reports that view.
-OPS_PER_BABY = 14
+# Roofline inputs, all committed measurements ("Roofline"):
+#  * profiles/r02_unit_counts.json: ncu counters of the walk kernels per d, per
+#    baby step and per giant step on the bench's scale (scripts/unit_counts.py);
+#  * profiles/r02_pipe_peaks.json: measured per-pipe issue peaks of this GPU
+#    model (bench_tools/pipe_peaks.cu), in warp-instructions per clock per SM.
+# SURVEY 8(d)'s basis for the issue roofline: 34 thread-instructions per
+# generic baby step plus c_g per giant step, c_g = the measured thread-
+# instructions of the giant + prep kernels per giant step.
 GENERIC_PER_BABY = 34
-OPS_PER_GIANT = 700    # thread-instructions of one fast-path giant step (K3 BSGS)
-OPS_PER_ENTRY = 12     # store insert per window entry: slot pack, hash, bucket insert
-# algorithmic HBM bytes of the window kernel (per-unit figures): per
-# entry 4 (list write) + 4 (list read-back by the build) + 64 / (16 * 0.62) (table
-# slots at load 0.62 in 64-byte buckets); per d 32 (window record) + 4 + 4 (offset,
-# queue entry)
-WIN_BYTES_PER_ENTRY = 4 + 4 + 64 / (16 * 0.62)
-WIN_BYTES_PER_D = 40
-# DRAM bytes per d of the BSGS walk at the bench configuration: dram__bytes_read +
-# dram__bytes_write of bsgs_window + bsgs_prep + bsgs_giant for one segment (ncu
-# --set full, profiles/r01_bsgs_walk.txt: 39.73 + 1.59 + 13.72 GB) / the segment's
-# 6.33 M d.  Algorithmic: list write + read-back 3.6 KB, table 2.9 KB, ~18.5 probes
-# x 64 B, records ~0.2 KB = ~7.9 KB per d.
-BSGS_DRAM_BYTES_PER_D = 8563
+UNIT_COUNTS = "profiles/r02_unit_counts.json"
+PIPE_PEAKS = "profiles/r02_pipe_peaks.json"
+ISSUE_WARP_PER_CLK_SM = 4.0          # one warp-instruction per clock per SMSP (pipe_peaks: FFMA 3.93)
+PIPE_OF_PEAK = {"alu": "IADD3", "fma": "FFMA", "fmaheavy": "IMAD", "fp64": "DFMA", "xu": "MUFU.RCP"}
+
+
+def _load_json(rel: str):
+    try:
+        with open(os.path.join(ROOT, rel)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
 
 
 def _env_int(k, d):
@@ -131,6 +131,16 @@ def measured_hbm_gbs() -> float:
         return 6650.0
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -153,7 +163,7 @@ def cpu_baseline(lo: int, hi: int, seconds_target: float = 15.0, n: int | None =
     f = c_oracle.classify_list(s, ncpu)
     dt = time.perf_counter() - t0
     nd = int((f != c_oracle.NOT_IN_D).sum())
-    return {"value": nd / dt, "unit": UNIT, "cores": ncpu, "kind": "oracle",
+    return {"value": nd / dt, "unit": UNIT, "cores": ncpu, "kind": "oracle", "cpu": cpu_model(),
             "sample": f"{len(s)} seeded uniform candidates (seed {workloads.SEED + 1}) of "
                       f"({lo}, {hi}], {nd} in D, big-integer CF oracle, {dt:.1f} s wall on "
                       f"{ncpu} threads"}
@@ -182,7 +192,7 @@ def run_reference(args) -> None:
         "config": {"workload": f"metric window ({lo}, {hi}]: all d = 5 mod 8 (oracle: seeded "
                                f"sample of {per_step} candidates per step)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": ncpu, "kind": "oracle",
-                         "sample": f"{per_step} seeded candidates of ({lo}, {hi}] per step"},
+                         "cpu": cpu_model(), "sample": f"{per_step} seeded candidates of ({lo}, {hi}] per step"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -198,6 +208,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--window-calls", type=int, default=5,
+                    help="one-call measurements of (9e9, 1e10] after the first (0: skip)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo: orchestration test only)")
     ap.add_argument("--share-gpu", action="store_true",
@@ -245,6 +257,30 @@ def main():
         allreduce_buckets(buckets)
         eis.prefix_dev(buckets, buckets, stream=stream)
 
+    # SURVEY 8(d)'s measurement form: one call over the whole window (9e9, 1e10]
+    # (checkpoints every 1e8) through the public API with host buffers; the
+    # first call of the process (scratch reservation, NCCL warm-up) is reported
+    # apart from the median of 5 later calls.  Wall clock around the synchronous
+    # call, max over ranks.
+    win_lo, win_hi = workloads.METRIC_TOP - 8 * workloads.METRIC_SLAB, workloads.METRIC_TOP
+    win_x = np.arange(win_lo + 10**8, win_hi + 1, 10**8, dtype=np.uint64)
+
+    def window_call() -> tuple[float, int, int]:
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if world > 1:
+            cD, cE = count_window_distributed(win_lo, win_x)
+        else:
+            cD, cE = eis.count_window(win_lo, win_x)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt[0]), int(cD[-1]), int(cE[-1])
+
+    first_call = window_call() if args.window_calls else None
+
     for _ in range(args.warmup):
         step()
         flush.fill_(1)
@@ -252,8 +288,8 @@ def main():
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    walk_ms, launches, stats = [], 0, {}
-    kern_ms = {"sieve": [], "window": [], "giant": []}
+    launches, stats = 0, {}
+    kern_ms = {"walk": [], "sieve": [], "window": [], "giant": []}
     cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
     sampler = ClockSampler(int(cvd.split(",")[gpu]) if cvd else gpu)
     sampler.start()
@@ -266,7 +302,6 @@ def main():
         step()
         ev[k][1].record(stream)
         stats = eis.get_stats()
-        walk_ms.append(stats["walk_ms"])
         for kn in kern_ms:
             kern_ms[kn].append(stats[f"{kn}_ms"])
         launches += int(stats["kernel_launches"]) + 1      # + prefix kernel
@@ -279,12 +314,12 @@ def main():
     tot_ms = sum(step_ms)
     res = buckets.cpu().numpy().astype(np.uint64)
 
-    t = torch.tensor([tot_ms, float(np.mean(walk_ms))] + [float(np.mean(v)) for v in kern_ms.values()],
+    t = torch.tensor([tot_ms] + [float(np.mean(v)) for v in kern_ms.values()],
                      dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tot_ms_max, walk_ms_max = float(t[0]), float(t[1])
-    kms = dict(zip(kern_ms, (float(v) for v in t[2:])))
+    tot_ms_max = float(t[0])
+    kms = dict(zip(kern_ms, (float(v) for v in t[1:])))
 
     # verification of the bench output itself: Table 1 window (9.9e9, 1e10]
     i99 = list(x).index(9_900_000_000)
@@ -310,45 +345,112 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ok = int(cD[-1]) == nD_job and int(cE[-1]) == int(res[2 * n - 1])
 
+    later_calls = [window_call() for _ in range(args.window_calls)]
+
     if rank == 0:
         value = nD_job / (tot_ms_max / args.steps / 1e3)
         sm_clk = clocks.get("sm_mhz") or SM_MAX_MHZ_FALLBACK
-        peak = 148 * 4 * 32 * sm_clk * 1e6 / 1e12                 # issue-slot peak, Tops/s
+        hz = sm_clk * 1e6
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        issue_peak_tops = nsm * ISSUE_WARP_PER_CLK_SM * 32 * hz / 1e12
         bsgs = stats["giant_steps"] > 0
-        # algorithmic thread-ops of each kernel family in one step (this rank)
-        entries = stats["baby_steps"] if bsgs else 0              # one store entry per step
-        kops = {"window": OPS_PER_BABY * stats["baby_steps"] + OPS_PER_ENTRY * entries,
-                "giant": OPS_PER_GIANT * stats["giant_steps"]}
-        per_kernel = {k: {"ms": kms[k], "tops": kops[k] / (kms[k] / 1e3) / 1e12 if kms[k] else None}
-                      for k in kops}
-        for k in per_kernel:
-            if per_kernel[k]["tops"] is not None:
-                per_kernel[k]["frac"] = per_kernel[k]["tops"] / peak
-        per_kernel["sieve"] = {"ms": kms["sieve"]}
+        uc = _load_json(UNIT_COUNTS) or {}
+        pk = _load_json(PIPE_PEAKS) or {}
+        kc = uc.get("kernels", {})
+        pipe_peak = {p: pk["ops"][op]["warp_inst_per_clk_per_sm"] for p, op in PIPE_OF_PEAK.items()
+                     if op in pk.get("ops", {})}
+        hbm_peak = measured_hbm_gbs()
+
+        def kernel_roof(names, ms):
+            """Per-pipe and issue utilisation of a kernel family over its live span:
+            ncu's per-d warp-instruction counts (UNIT_COUNTS, the bench's scale) x
+            the d this rank classified per step / the live span, against the
+            measured per-pipe peaks (PIPE_PEAKS) at the sampled SM clock."""
+            if not ms or not all(nm in kc for nm in names):
+                return None
+            sec = ms / 1e3
+            warp = sum(kc[nm]["warp_inst_per_d"] for nm in names) * nD_rank
+            out = {"ms": ms, "issue": warp / sec / (nsm * ISSUE_WARP_PER_CLK_SM * hz),
+                   "threads_per_inst": sum(kc[nm]["thread_inst_per_d"] for nm in names) * nD_rank / warp,
+                   "pipes": {}}
+            for p, peak in pipe_peak.items():
+                w = sum(kc[nm]["pipe_warp_inst_per_d"][p] for nm in names) * nD_rank
+                out["pipes"][p] = w / sec / (nsm * peak * hz)
+            dram = sum(kc[nm]["dram_bytes_per_d"] for nm in names) * nD_rank
+            out["hbm_measured_bytes"] = dram / sec / 1e9 / hbm_peak
+            top = max(out["pipes"].items(), key=lambda kv: kv[1]) if out["pipes"] else ("-", 0)
+            out["top_pipe"] = {"pipe": top[0], "frac": top[1]}
+            return out
+
+        per_kernel = {"sieve": {"ms": kms["sieve"]}}
+        roofline = {}
         if bsgs:
-            # the window kernel is bound by HBM, not issue: its algorithmic bytes over
-            # its live span (which overlaps the giant kernel of the previous segment)
-            wbytes = WIN_BYTES_PER_ENTRY * entries + WIN_BYTES_PER_D * stats["d_classified"]
-            hbm_peak = measured_hbm_gbs()
-            per_kernel["window"]["hbm"] = {
-                "bytes_per_step": wbytes, "gbs": wbytes / (kms["window"] / 1e3) / 1e9,
-                "peak_gbs": hbm_peak, "frac": wbytes / (kms["window"] / 1e3) / 1e9 / hbm_peak,
-                "note": "live span includes the overlapped giant kernel; ncu alone "
-                        "(profiles/r01_bsgs_walk.txt): 39.7 GB in 7.22 ms per 6.33 M-d "
-                        "segment = 5.5 TB/s, 0.84 of the measured copy bandwidth"}
-        if bsgs:
-            # the BSGS kernels run on two streams and overlap (the giant kernel of one
-            # segment with the window kernel of the next), so the walk is the unit:
-            # all of its algorithmic ops over its device time
-            ops_per_launch = kops["window"] + kops["giant"]
-            achieved = ops_per_launch / (walk_ms_max / 1e3) / 1e12
-            dom_name = "BSGS walk: bsgs_window_kernel + bsgs_prep_kernel + bsgs_giant_kernel"
-            dom_ms = walk_ms_max
+            per_kernel["window"] = kernel_roof(["bsgs_window_kernel", "bsgs_prep_kernel"], kms["window"])
+            per_kernel["giant"] = kernel_roof(["bsgs_giant_kernel"], kms["giant"])
+            # the dominant kernel (the window kernel: the largest share of the
+            # serialised launch list, profiles/r02_*) is bound by HBM first:
+            # ncu puts its DRAM traffic at ~0.8 of the measured copy bandwidth,
+            # above its issue (~0.7) and any pipe (ALU ~0.55).  achieved =
+            # ALGORITHMIC bytes (SURVEY 8(d): the per-d store) per launch over
+            # the launch's live duration: list 4 nw + table 64 nb + records 40
+            # bytes per windowed d (nw, nb from the library's plan).
+            nw, nb = stats["window_nw"], stats["window_nb"]
+            alg = (4 * nw + 64 * nb + 40) * stats["windowed"]
+            wl = max(1, int(stats["kernel_launches"]) // 4)     # sieve, window, prep, giant per segment
+            traffic = (kc["bsgs_window_kernel"]["dram_bytes_per_d"] * nD_rank / wl
+                       if "bsgs_window_kernel" in kc else None)
+            achieved = alg / (kms["window"] / 1e3) / 1e9
+            roofline = {
+                "bound": "hbm", "kernel": "bsgs_window_kernel (+ bsgs_prep_kernel in its span)",
+                "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic,
+                "basis": f"algorithmic bytes per windowed d = 4 nw + 64 nb + 40 (list, table, "
+                         f"records; nw={nw}, nb={nb}) x {stats['windowed']} d per step over the "
+                         f"live window span (CUDA events on its stream, {wl} launches per step); "
+                         f"peak = measured copy bandwidth (MEASURED_PEAKS.json); traffic = ncu "
+                         f"dram read+write per launch ({UNIT_COUNTS}); the list read-back by the "
+                         f"store build is not algorithmic (it mostly misses L2)",
+            }
+            # SURVEY 8(d)'s issue roofline of the whole walk (three kernels on two
+            # streams): 34 per baby step + c_g per giant step over the walk's span
+            cg = None
+            if "bsgs_giant_kernel" in kc and uc.get("giant_steps"):
+                cg = ((kc["bsgs_giant_kernel"]["thread_inst_per_d"] +
+                       kc["bsgs_prep_kernel"]["thread_inst_per_d"]) * uc["d"] / uc["giant_steps"])
+            if cg:
+                ops = GENERIC_PER_BABY * stats["baby_steps"] + cg * stats["giant_steps"]
+                a_t = ops / (kms["walk"] / 1e3) / 1e12
+                roofline["walk_issue"] = {
+                    "achieved": a_t, "peak": issue_peak_tops, "unit": "T thread-ops/s",
+                    "frac": a_t / issue_peak_tops,
+                    "basis": f"{GENERIC_PER_BABY} per baby step + c_g = {cg:.0f} per giant step "
+                             f"(measured: giant + prep thread-instructions per giant step, "
+                             f"{UNIT_COUNTS}) over the walk's live span; peak = {nsm} SM x "
+                             f"{ISSUE_WARP_PER_CLK_SM:.0f} warp-inst/clk x 32 at the sampled "
+                             f"{sm_clk:.0f} MHz (FFMA alone issues 3.93 of the 4 per clock, {PIPE_PEAKS})"}
         else:
-            ops_per_launch = kops["window"]
-            achieved = per_kernel["window"]["tops"]
-            dom_name = "walk_half_kernel"
-            dom_ms = kms["window"]
+            per_kernel["half"] = {"ms": kms["window"]}
+            ops = 14 * stats["baby_steps"]
+            a_t = ops / (kms["window"] / 1e3) / 1e12
+            roofline = {"bound": "issue", "kernel": "walk_half_kernel", "achieved": a_t,
+                        "peak": issue_peak_tops, "unit": "T thread-ops/s", "frac": a_t / issue_peak_tops,
+                        "traffic": None, "basis": "14 thread-instructions per rho step (DESIGN.md 4)"}
+        roofline["per_kernel"] = per_kernel
+        roofline["walk_ms_per_step"] = kms["walk"]
+        roofline["walk_share_of_step"] = kms["walk"] / (tot_ms_max / args.steps)
+        window_field = None
+        if first_call is not None:
+            nD_win = first_call[1]
+            med = statistics.median(c[0] for c in later_calls) if later_calls else None
+            window_field = {
+                "range": f"({win_lo}, {win_hi}]", "checkpoints": len(win_x), "d": nD_win,
+                "E": first_call[2], "first_call_s": first_call[0],
+                "first_call_rate": nD_win / first_call[0],
+                "median_s": med, "median_rate": nD_win / med if med else None,
+                "calls": len(later_calls),
+                "path": "eis_count_window (host buffers)" if world == 1 else
+                        "count_window_distributed (C ABI dev + all-reduce)",
+                "consistent": all(c[1] == nD_win and c[2] == first_call[2] for c in later_calls)}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -370,35 +472,11 @@ def main():
                     "path": "eis_count_window (C ABI, host buffers)" if world == 1
                     else f"count_window_distributed (C ABI dev + {args.backend} allreduce)"},
             "gpu_launches": launches,
-            "roofline": {
-                "bound": "alu", "kernel": dom_name,
-                "achieved": achieved, "peak": peak, "unit": "Tops/s", "frac": achieved / peak,
-                "traffic": BSGS_DRAM_BYTES_PER_D * nD_rank if bsgs else 50.8e6,
-                "traffic_note": ("dram read+write bytes per step of the BSGS walk: 8.56 KB per d "
-                                 "measured by ncu --set full on the bench workload "
-                                 "(profiles/r01_bsgs_walk.txt) x d per step; algorithmic ~8.5 KB "
-                                 "per d (list 3.9, table 3.2, probes 1.1, records 0.3); the "
-                                 "window kernel is HBM-bound (per_kernel.window.hbm), the giant "
-                                 "kernel issue/latency-bound") if bsgs else
-                                "dram read+write bytes per walk launch, ncu --set full "
-                                "(profiles/r01_half_walk.txt); algorithmic bytes = 4 per d "
-                                "(survivor list) = 50.7 MB",
-                "ops_per_step": ops_per_launch,
-                "kernel_ms_per_step": dom_ms,
-                "per_kernel": per_kernel,
-                "work_equiv_generic": None if bsgs else
-                (GENERIC_PER_BABY * stats["baby_steps"]) / (kms["window"] / 1e3) / 1e12 / peak,
-                "walk_ms_per_step": walk_ms_max,
-                "walk_share_of_step": walk_ms_max / (tot_ms_max / args.steps),
-                "basis": f"thread-ops per unit: {OPS_PER_BABY} per rho step, {OPS_PER_ENTRY} per "
-                         f"store entry, {OPS_PER_GIANT} per giant step; kernel time = summed CUDA "
-                         f"events around its launches on its own stream (BSGS: the walk's span, "
-                         f"per_kernel spans overlap); peak = 148 SM x 4 SMSP x "
-                         f"32 lanes x {sm_clk:.0f} MHz (sampled SM clock) issue slots (DESIGN.md 4)",
-            },
+            "roofline": roofline,
+            "window_call": window_field,
             "clocks": clocks,
             "stats_per_rank_step": {k: stats[k] for k in ("d_classified", "baby_steps",
-                                                          "giant_steps", "sym_exits")},
+                                                          "giant_steps", "sym_exits", "windowed")},
             "rank_d": nD_rank,
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -237,9 +237,13 @@ typedef struct {
     double sieve_ms;         /* summed device time of the sieve kernels (events on their stream) */
     double window_ms;        /* ... of the HALF walk kernels, or of the BSGS window + prep kernels */
     double giant_ms;         /* ... of the BSGS giant kernels (aux stream; overlaps the others) */
+    uint64_t windowed;       /* d whose BSGS window (list + hash table) was stored */
+    uint64_t window_nw;      /* window entries per d of the last BSGS segment (0: none) */
+    uint64_t window_nb;      /* table buckets (64 bytes each) per d of the last BSGS segment */
 } eis_stats;
 
-/* Counters of the most recent compute call (synchronises the device). */
+/* Counters of the most recent compute call (a copy of host-side values the
+ * call recorded when it finished; no device work). */
 EIS_API int eis_get_stats(eis_stats *out);
 
 #ifdef __cplusplus

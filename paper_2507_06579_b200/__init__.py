@@ -67,6 +67,9 @@ class Stats(ctypes.Structure):
         ("sieve_ms", ctypes.c_double),
         ("window_ms", ctypes.c_double),
         ("giant_ms", ctypes.c_double),
+        ("windowed", ctypes.c_uint64),
+        ("window_nw", ctypes.c_uint64),
+        ("window_nb", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:

@@ -23,6 +23,15 @@ typedef uint16_t u16;
 // rare paths kept out of line (smaller hot loops, fewer instruction-cache misses)
 #define EIS_HD_COLD __host__ __device__ __noinline__
 
+// Host-only event counters for the CPU emulation's per-step profile
+// (tests/emu, -DEIS_HOST_PROFILE); compiled out everywhere else.
+#if defined(EIS_HOST_PROFILE) && !defined(__CUDA_ARCH__)
+extern unsigned eis_prof[16];
+#define EIS_PROF(i) (void)(eis_prof[i]++)
+#else
+#define EIS_PROF(i) (void)0
+#endif
+
 // fast reciprocal: MUFU.RCP on the device; IEEE 1/x in the host emulation
 // (both are within the 2^-22 relative error the quotient proofs assume)
 EIS_HD float rcp_approx(float x) {
@@ -155,6 +164,7 @@ struct WalkArgs {
 
 enum EisStatSlot {
     ST_D = 0, ST_BABY = 1, ST_GIANT = 2, ST_REDUCE = 3, ST_SYM = 4, ST_FALLBACK = 5,
+    ST_WINDOWED = 6,     // d whose BSGS window (list + table) was stored
     ST_NSLOTS = 8
 };
 

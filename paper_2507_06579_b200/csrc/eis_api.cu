@@ -78,6 +78,7 @@ struct Ctx {
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
+    int last_nw = 0, last_nb = 0;    // window entries / table buckets per d of the last BSGS segment
     int launches = 0;
     // per-kernel device time: event pairs around each launch, summed at the end
     // of run_range (the events are complete then)
@@ -367,6 +368,8 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
+            g.last_nw = pl.B.nw;
+            g.last_nb = pl.B.nb;
             CUDA_TRY(cudaEventRecord(kev_next(e0), s));
             if (bsgs_launch_baby(a, pl, s))
                 return fail(EIS_EDEVICE, "BSGS baby launch failed: %s",
@@ -461,6 +464,7 @@ __global__ void prefix_kernel(const u64 *in, u64 *out, int n, int nrow) {
 
 int begin_call(cudaStream_t s) {
     g.walk_ms_acc = 0;
+    g.last_nw = g.last_nb = 0;
     g.launches = 0;
     g.kms[0] = g.kms[1] = g.kms[2] = 0;
     CUDA_TRY(cudaMemsetAsync(g.d_stats, 0, ST_NSLOTS * sizeof(u64), s));
@@ -488,6 +492,9 @@ int end_call(cudaStream_t s) {
     g.last.sieve_ms = g.kms[0];
     g.last.window_ms = g.kms[1];
     g.last.giant_ms = g.kms[2];
+    g.last.windowed = st[ST_WINDOWED];
+    g.last.window_nw = (u64)g.last_nw;
+    g.last.window_nb = (u64)g.last_nb;
     return 0;
 }
 

@@ -125,6 +125,7 @@ constexpr float RMAGIC = 12582912.0f;  // 1.5 * 2^23: round to nearest for |v| <
 EIS_HD float fxgcd_x(float a, float b, float &x) {
     float x0 = 1.f, x1 = 0.f;
     while (b != 0.f) {
+        EIS_PROF(0);
         const float q = fmaf(a, rcp_approx(b), RMAGIC) - RMAGIC;
         const float r = fmaf(-q, b, a);
         a = b;
@@ -444,6 +445,7 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     warp_reconverge(wmask);
     double G = 1.0, By = u1, Cy = u2, Dy = s, rBy;
     float fbx0;
+    EIS_PROF(4);
     if (F == 1.f) {                            // gcd(u1, u2) = 1: G = 1, Bx = m b
         rBy = rcp64(By);
         fbx0 = (float)dfloor_mod(m * (double)fb, By, rBy);      // |m b| < 2^39
@@ -457,9 +459,11 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
         Cy = rint(u2 * rG);
         Dy = rint(s * rG);
         rBy = rcp64(By);
+        EIS_PROF(5);
         if (Gf == F) {                         // F | s: G = F, Bx = m b
             fbx0 = (float)dfloor_mod(m * (double)fb, By, rBy);
         } else {                               // Alg. 2 l.630-634, all reduced mod H first
+            EIS_PROF(1);
             const double H = rint((double)F * rG), rH = rcp64(H);
             const double b = fb;
             const double c = dexact_div(fma(-b, u2, (double)F), u1, rcp64(u1), err);
@@ -476,6 +480,7 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     float fbx = fbx0, fby = (float)By, fx = 1.f, fy = 0.f;
     int z = 0;
     while (fby > L && fbx != 0.f) {
+        EIS_PROF(2);
         const float q = ffloor_div_pos(fby, fbx);
         const float t = fmaf(-q, fbx, fby);
         fby = fbx;
@@ -488,6 +493,8 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     if (z & 1) { fby = -fby; fy = -fy; }
     warp_reconverge(wmask);
     const double bx = fbx, by = fby, x = fx, y = fy;
+    if (z == 0) EIS_PROF(6);
+    if (bx == 0.0) EIS_PROF(7);
     if (z != 0) {
         const double cx = dexact_div(fma(Cy, bx, -m * x), By, rBy, err);
         const double Q1 = by * cx;
@@ -592,6 +599,7 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     const u32 fmask = warp_ballot(wmask, !rare && !fdup);
     const u32 dmask = dup_fast ? warp_ballot(wmask, fdup) : 0u;
     if (rare) {
+        EIS_PROF(8);
         const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
         r.Q = c.Q;
         r.P = s - floor_mod(s - c.P, c.Q);

@@ -205,6 +205,7 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
         const bool full = bucket_slot(p, BKT - 1) != 0;
         if (qk == 0) mm &= filled_mask(p);
         while (mm) {
+            EIS_PROF(9);
             const int i = __builtin_ctz_portable(mm);
             mm &= mm - 1;
             const u32 e = tab[(size_t)p.b * BKT + i];
@@ -218,6 +219,7 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
             }
         }
         if (!full) return HIT_NONE;
+        EIS_PROF(10);
         load_bucket(tab, next_bucket(p.b, nb), p);       // bucket full: continue
     }
 }
@@ -412,6 +414,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
         double Cd = rint((double)(d - P * P) * rQ);
         double mag = 1.0;                               // prod |P' + sqrt d| / Q
         do {
+            EIS_PROF(3);
             const double num = Pd + sd;
             double q = floor(num * rQ);              // floor((P + sqrt d)/Q)
             const double rr = fma(-q, Qd, num);
@@ -608,11 +611,11 @@ __device__ __forceinline__ void record_result(const WalkArgs &a, u32 *hist, u32 
 }
 
 __device__ __forceinline__ void flush_stats(const WalkArgs &a, u64 baby, u64 giant, u64 red,
-                                            u64 done, u64 sym, u64 fb, u32 err) {
+                                            u64 done, u64 sym, u64 fb, u32 err, u64 win = 0) {
     const int lane = threadIdx.x & 31;
     const u64 s_baby = warp_sum_u64(baby), s_giant = warp_sum_u64(giant),
               s_red = warp_sum_u64(red), s_done = warp_sum_u64(done), s_sym = warp_sum_u64(sym),
-              s_fb = warp_sum_u64(fb);
+              s_fb = warp_sum_u64(fb), s_win = warp_sum_u64(win);
     const u32 s_err = __reduce_add_sync(FULL_MASK, err);
     if (lane == 0 && a.stats) {
         atomicAdd((unsigned long long *)&a.stats[ST_BABY], (unsigned long long)s_baby);
@@ -621,6 +624,7 @@ __device__ __forceinline__ void flush_stats(const WalkArgs &a, u64 baby, u64 gia
         atomicAdd((unsigned long long *)&a.stats[ST_D], (unsigned long long)s_done);
         atomicAdd((unsigned long long *)&a.stats[ST_SYM], (unsigned long long)s_sym);
         atomicAdd((unsigned long long *)&a.stats[ST_FALLBACK], (unsigned long long)s_fb);
+        if (s_win) atomicAdd((unsigned long long *)&a.stats[ST_WINDOWED], (unsigned long long)s_win);
     }
     if (lane == 0 && s_err) atomicAdd(a.err, s_err);
 }
@@ -834,7 +838,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     __syncthreads();
     const u32 n = *a.count;
     const int nblk = B.nw / 8;
-    u32 baby = 0, done = 0, sym = 0;                    // per-thread counts fit in 32 bits
+    u32 baby = 0, done = 0, sym = 0, win = 0;           // per-thread counts fit in 32 bits
     for (;;) {
         u32 wave = 0;
         if (lane == 0) wave = atomicAdd(a.work, 1u);
@@ -880,7 +884,10 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             done++;
             sym++;
         }
-        if (w.live) o.brecs[idx] = win_pack(w, __ldg(a.list + idx), (u32)B.nw);
+        if (w.live) {
+            o.brecs[idx] = win_pack(w, __ldg(a.list + idx), (u32)B.nw);
+            win++;
+        }
         const u32 live = __ballot_sync(FULL_MASK, w.live);
         uint4 nx[BUILD_K];
         if (live)
@@ -898,7 +905,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         qb = __shfl_sync(FULL_MASK, qb, 0);
         if (w.live) o.bqueue[qb + __popc(live & lanemask_lt())] = idx;
     }
-    flush_stats(a, baby, 0, 0, done, sym, 0, 0);
+    flush_stats(a, baby, 0, 0, done, sym, 0, 0, win);
     hist_flush(a, hist);
 }
 
