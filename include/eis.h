@@ -25,9 +25,11 @@
  *  - Host pointers are owned by the caller and only read/written during the
  *    call (the call is synchronous).  Device pointers (the *_dev variants) are
  *    owned by the caller, must be device memory on the library's current
- *    device, and are accessed asynchronously on `stream` (a cudaStream_t
- *    passed as void*; NULL = the legacy default stream); the caller
- *    synchronises.
+ *    device, and are written by kernels on `stream` (a cudaStream_t passed as
+ *    void*; NULL = the legacy default stream).  eis_count_buckets_dev and
+ *    eis_classify_range_dev return only after their kernels have finished
+ *    (they read back an invariant-violation counter); eis_prefix_dev is
+ *    asynchronous (the caller synchronises).
  *  - The library owns its device scratch (prime table, survivor lists,
  *    counters) until eis_finalize().
  *  - Calls are NOT reentrant and not thread-safe: serialise them per process.
@@ -112,7 +114,9 @@ EIS_API int64_t eis_get_option(const char *key);
 /* Number of candidates d = 5 (mod 8) with lo <= d <= hi (0 if lo > hi). */
 EIS_API size_t eis_num_candidates(uint64_t lo, uint64_t hi);
 
-/* Per-d classification.
+/* Per-d classification.  Slices of 2^segment_log2
+ * candidates are classified in turn; each slice's device-to-host copy overlaps
+ * the next slice's kernels (two device buffers, a copy stream).
  * out[i] describes d_i = first + 8 i, first = least d >= lo with d = 5 mod 8,
  * for every d_i <= hi: out[i] = t(eps_{d_i}) in {0,1,2} (d_i in E iff 0),
  * or EIS_NOT_IN_D if d_i is not squarefree.
@@ -165,7 +169,8 @@ EIS_API int eis_count_buckets_dev(uint64_t lo, uint64_t hi, const uint64_t *x, s
  * Async on `stream`; out_dev may equal bucket_dev. */
 EIS_API int eis_prefix_dev(const uint64_t *bucket_dev, size_t n, uint64_t *out_dev, void *stream);
 
-/* eis_classify_range into device memory out_dev (out_len bytes), async. */
+/* eis_classify_range into device memory out_dev (out_len bytes), on `stream`;
+ * returns after the kernels finished (host-blocking, like eis_count_buckets_dev). */
 EIS_API int eis_classify_range_dev(uint64_t lo, uint64_t hi, uint8_t *out_dev, size_t out_len,
                            void *stream);
 

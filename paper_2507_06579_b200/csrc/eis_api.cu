@@ -54,7 +54,13 @@ struct Ctx {
     u64 *d_stats = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;      // giant kernels
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool walk_open = false;          // ev[2] marks the start of an unfinished run_range sequence
+    // eis_classify_range: two flag buffers, their D2H copies on a copy stream
+    u8 *d_flags2[2] = {nullptr, nullptr};
+    size_t flags2_cap = 0;
+    cudaStream_t cpy = nullptr;
+    cudaEvent_t fl_ready[2] = {nullptr, nullptr}, fl_free[2] = {nullptr, nullptr};
     // whole box (eis_comm_init): NCCL communicator over one process per GPU
     ncclComm_t comm = nullptr;
     int comm_world = 1, comm_rank = 0;
@@ -102,6 +108,7 @@ cudaEvent_t kev_next(int &idx) {
     return g.kev[idx];
 }
 
+const char *eis_last_error_internal();
 int fail(int code, const char *fmt, ...) {
     char buf[512];
     va_list ap;
@@ -120,6 +127,12 @@ int fail(int code, const char *fmt, ...) {
                         "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
                         __LINE__);                                                         \
     } while (0)
+
+const char *eis_last_error_internal() {
+    static thread_local std::string copy;
+    copy = g_err;
+    return copy.c_str();
+}
 
 u64 isqrt_host(u64 n) {
     u64 s = (u64)std::sqrt((double)n);
@@ -180,6 +193,11 @@ int do_init(int device) {
     CUDA_TRY(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&g.aux, cudaStreamNonBlocking));
     for (auto &ev : g.ev) CUDA_TRY(cudaEventCreate(&ev));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.cpy, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; k++) {
+        CUDA_TRY(cudaEventCreateWithFlags(&g.fl_ready[k], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&g.fl_free[k], cudaEventDisableTiming));
+    }
     CUDA_TRY(cudaFuncSetAttribute(sieve_compact_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   2 * SIEVE_WORDS * (int)sizeof(u32)));
@@ -230,16 +248,50 @@ bool want_bsgs(u64 d_lo) {
 
 // Process candidates [i_first, i_last].  flags_dev (nullable) is indexed by
 // candidate index - i_first.  x_host/x_dev/n/buckets_dev (nullable) receive counts.
+// The end of a sequence of run_range(..., finish = false) calls: wait for the
+// streams, add the segment loop's and the kernels' device times to the call's
+// statistics, and fail the call if any kernel counted an invariant violation.
+int finish_range(cudaStream_t s) {
+    if (g.walk_open) {
+        CUDA_TRY(cudaEventRecord(g.ev[3], s));
+        CUDA_TRY(cudaEventSynchronize(g.ev[3]));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, g.ev[2], g.ev[3]);
+        g.walk_ms_acc += ms;
+        g.walk_open = false;
+    }
+    for (int k = 0; k < 3; k++) {
+        for (auto &pr : g.kspan[k]) {
+            float t = 0;
+            if (cudaEventElapsedTime(&t, g.kev[pr.first], g.kev[pr.second]) == cudaSuccess)
+                g.kms[k] += t;
+        }
+        g.kspan[k].clear();
+    }
+    g.kev_used = 0;
+    u32 err = 0;
+    CUDA_TRY(cudaMemcpy(&err, g.d_err, sizeof(u32), cudaMemcpyDeviceToHost));
+    if (err) return fail(EIS_EINTERNAL, "%u in-kernel invariant violations", err);
+    return 0;
+}
+
+// Process candidates [i_first, i_last].  flags_dev (nullable) is indexed by
+// candidate index - i_first.  x_host/x_dev/n/buckets_dev (nullable) receive counts.
+// finish = false leaves the kernels queued (no host wait); the caller then
+// calls finish_range.
 int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u64 *x_dev,
-              int n, u64 *buckets_dev, cudaStream_t s, int nrow = 2) {
+              int n, u64 *buckets_dev, cudaStream_t s, int nrow = 2, bool finish = true) {
     // AUTO: a range that spans the crossover runs as two ranges (HALF below, BSGS
     // at and above it)
     if (g.mode == EIS_MODE_AUTO && cand_d(i_first) < g.crossover && cand_d(i_last) >= g.crossover) {
         const u64 i_cross = (g.crossover - 5 + 7) / 8;     // least i with 8i + 5 >= crossover
-        if (int rc = run_range(i_first, i_cross - 1, flags_dev, x_host, x_dev, n, buckets_dev, s, nrow))
+        if (int rc = run_range(i_first, i_cross - 1, flags_dev, x_host, x_dev, n, buckets_dev, s,
+                               nrow, false))
             return rc;
-        return run_range(i_cross, i_last, flags_dev ? flags_dev + (i_cross - i_first) : nullptr,
-                         x_host, x_dev, n, buckets_dev, s, nrow);
+        if (int rc = run_range(i_cross, i_last, flags_dev ? flags_dev + (i_cross - i_first) : nullptr,
+                               x_host, x_dev, n, buckets_dev, s, nrow, false))
+            return rc;
+        return finish ? finish_range(s) : 0;
     }
     const int with_primes = nrow > 2;
     const u64 SEG = 1ull << g.segment_log2;
@@ -292,7 +344,10 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
             seg_cap = std::max<u64>((total + nseg - 1) / nseg, 1ull << 16);
         }
     }
-    CUDA_TRY(cudaEventRecord(g.ev[2], s));
+    if (!g.walk_open) {
+        CUDA_TRY(cudaEventRecord(g.ev[2], s));
+        g.walk_open = true;
+    }
     int iseg = 0;
     bool used_aux = false;
     for (u64 seg = i_first; seg <= i_last; iseg++) {
@@ -413,27 +468,15 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         seg += len;
     }
     if (used_aux) {                                   // join the aux stream back into s
-        CUDA_TRY(cudaEventRecord(g.ev[3], g.aux));
-        CUDA_TRY(cudaStreamWaitEvent(s, g.ev[3], 0));
+        CUDA_TRY(cudaEventRecord(g.ev[4], g.aux));
+        CUDA_TRY(cudaStreamWaitEvent(s, g.ev[4], 0));
     }
-    CUDA_TRY(cudaEventRecord(g.ev[3], s));
-    CUDA_TRY(cudaEventSynchronize(g.ev[3]));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, g.ev[2], g.ev[3]);
-    g.walk_ms_acc += ms;
-    for (int k = 0; k < 3; k++) {
-        for (auto &pr : g.kspan[k]) {
-            float t = 0;
-            if (cudaEventElapsedTime(&t, g.kev[pr.first], g.kev[pr.second]) == cudaSuccess)
-                g.kms[k] += t;
-        }
-        g.kspan[k].clear();
-    }
-    g.kev_used = 0;
-    u32 err = 0;
-    CUDA_TRY(cudaMemcpy(&err, g.d_err, sizeof(u32), cudaMemcpyDeviceToHost));
-    if (err) return fail(EIS_EINTERNAL, "%u in-kernel invariant violations in [%llu, %llu]", err,
-                         (unsigned long long)cand_d(i_first), (unsigned long long)cand_d(i_last));
+    if (!finish) return 0;
+    if (int rc = finish_range(s))
+        return rc == EIS_EINTERNAL
+                   ? fail(EIS_EINTERNAL, "%s in [%llu, %llu]", eis_last_error_internal(),
+                          (unsigned long long)cand_d(i_first), (unsigned long long)cand_d(i_last))
+                   : rc;
     return 0;
 }
 
@@ -464,6 +507,7 @@ __global__ void prefix_kernel(const u64 *in, u64 *out, int n, int nrow) {
 
 int begin_call(cudaStream_t s) {
     g.walk_ms_acc = 0;
+    g.walk_open = false;
     g.last_nw = g.last_nb = 0;
     g.launches = 0;
     g.kms[0] = g.kms[1] = g.kms[2] = 0;
@@ -671,6 +715,12 @@ void eis_finalize(void) {
     cudaFree(g.d_buckets);
     cudaFree(g.d_stats);
     for (auto &ev : g.ev) if (ev) cudaEventDestroy(ev);
+    for (int k = 0; k < 2; k++) {
+        cudaFree(g.d_flags2[k]);
+        if (g.fl_ready[k]) cudaEventDestroy(g.fl_ready[k]);
+        if (g.fl_free[k]) cudaEventDestroy(g.fl_free[k]);
+    }
+    if (g.cpy) cudaStreamDestroy(g.cpy);
     for (auto &ev : g.kev) cudaEventDestroy(ev);
     if (g.stream) cudaStreamDestroy(g.stream);
     if (g.aux) cudaStreamDestroy(g.aux);
@@ -787,15 +837,42 @@ int eis_classify_range(uint64_t lo, uint64_t hi, uint8_t *out, size_t out_len) {
     if (int rc = begin_call(s)) return rc;
     u64 a, b;
     cand_range(lo, hi, a, b);
+    // Flags of slice k go to device buffer k & 1; its D2H copy (copy stream)
+    // overlaps slice k+1's kernels: slice k+1 is queued before the host issues
+    // (and, for pageable `out`, waits for) slice k's copy.
     const u64 SEG = 1ull << g.segment_log2;
-    if (ensure(g.d_flags, g.flags_cap, (size_t)std::min<u64>(SEG, n))) return EIS_ENOMEM;
-    for (u64 seg = a; seg <= b; seg += SEG) {
-        u64 e = std::min(b, seg + SEG - 1);
-        if (int rc = run_range(seg, e, g.d_flags, nullptr, nullptr, 0, nullptr, s)) return rc;
-        CUDA_TRY(cudaMemcpyAsync(out + (seg - a), g.d_flags, (size_t)(e - seg + 1),
-                                 cudaMemcpyDeviceToHost, s));
+    const size_t cap = (size_t)std::min<u64>(SEG, n);
+    if (g.flags2_cap < cap) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        for (auto &p : g.d_flags2) { cudaFree(p); p = nullptr; }
+        g.flags2_cap = 0;
+        for (auto &p : g.d_flags2) CUDA_TRY(cudaMalloc(&p, cap));
+        g.flags2_cap = cap;
     }
-    CUDA_TRY(cudaStreamSynchronize(s));
+    u64 prev = ~0ull, prev_e = 0;
+    int k = 0;
+    auto copy_out = [&](u64 seg, u64 e, int buf) -> int {
+        CUDA_TRY(cudaStreamWaitEvent(g.cpy, g.fl_ready[buf], 0));
+        CUDA_TRY(cudaMemcpyAsync(out + (seg - a), g.d_flags2[buf], (size_t)(e - seg + 1),
+                                 cudaMemcpyDeviceToHost, g.cpy));
+        CUDA_TRY(cudaEventRecord(g.fl_free[buf], g.cpy));
+        return 0;
+    };
+    for (u64 seg = a; seg <= b; seg += SEG, k++) {
+        const u64 e = std::min(b, seg + SEG - 1);
+        const int buf = k & 1;
+        if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(s, g.fl_free[buf], 0));   // its last copy is done
+        if (int rc = run_range(seg, e, g.d_flags2[buf], nullptr, nullptr, 0, nullptr, s, 2, false))
+            return rc;
+        CUDA_TRY(cudaEventRecord(g.fl_ready[buf], s));
+        if (prev != ~0ull)
+            if (int rc = copy_out(prev, prev_e, buf ^ 1)) return rc;
+        prev = seg;
+        prev_e = e;
+    }
+    if (int rc = copy_out(prev, prev_e, (k - 1) & 1)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(g.cpy));
+    if (int rc = finish_range(s)) return rc;
     return end_call(s);
 }
 

@@ -39,6 +39,20 @@ EIS_HD double rcp64(double b) {
 #endif
 }
 
+// 1/b with one Newton step from the MUFU.RCP64H seed (relative error ~2^-40):
+// enough wherever a floor or rint of n * r is corrected by one exact remainder
+// test or the quotient stays below ~2^38 (the rho loop of giant_advance).
+EIS_HD double rcp64_1(double b) {
+#ifdef __CUDA_ARCH__
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    const double e = fma(-b, r, 1.0);
+    return fma(r, e, r);
+#else
+    return 1.0 / b;
+#endif
+}
+
 // floor(a / b) for b > 0, |a| < 2^62, |a/b| < 2^50: double estimate, one
 // integer correction each way.
 EIS_HD i64 floor_div(i64 a, i64 b) {

@@ -76,9 +76,6 @@ EIS_HD int __double2loint_hd(double x) {          // the low 32 bits of x's enco
     return (int)(u32)b;
 #endif
 }
-#ifndef RHO_CARRY_C
-#define RHO_CARRY_C 1                 // giant_advance's rho loop carries C = (d - P^2)/Q
-#endif
 EIS_HD u32 mod3_small(u32 v) { return v - 3u * ((v * 0x5556u) >> 16); }   // v < 2^15
 
 // Two-sided window (R35).  Conjugation reverses the principal cycle
@@ -397,7 +394,6 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
     i64 Q = c.Q, P = c.P;                        // P canonical in (s - Q, s]
     u32 nred = 0;
     if (Q - P > s) {                             // not reduced (R18): apply rho
-#if RHO_CARRY_C
         // Exact fp64 integers, carrying the third coefficient C = (d - P^2)/Q of
         // the ideal (Q, P) so that no step forms d - P'^2 (|P'| reaches 2^28, so
         // that needs int64): rho gives P' = qQ - P, Q' = C + q (P - P'), C' = Q,
@@ -408,7 +404,7 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
         // of P' is read from the low word of P' + 1.5 * 2^52 (no conversion), and
         // the distance is accumulated as a product, with one log at the end.
         const double sd = (double)s;
-        double Qd = (double)Q, Pd = (double)P, rQ = rcp64(Qd);
+        double Qd = (double)Q, Pd = (double)P, rQ = rcp64_1(Qd);
         // C = (d - P^2)/Q: |P| < Q + s may reach 2^28, so d - P^2 in int64; the
         // quotient is < 2^37 and the division exact, so rint recovers it
         double Cd = rint((double)(d - P * P) * rQ);
@@ -422,12 +418,12 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
             const double Pn = fma(q, Qd, -Pd);
             double Qn = fma(q, Pd - Pn, Cd);
             const u32 plo = (u32)__double2loint_hd(Pn + 6755399441055744.0);   // P' mod 2^32
-            t = mod3_small(t + 1u + ((plo >> 1) & 1u));
+            t += 1u + ((plo >> 1) & 1u);             // (reduced mod 3 after the loop)
             mag *= fabs(Pn + (double)g.sqrtd) * rQ;
             Cd = Qd;                                  // C' = Q
             if (Qn < 0.0) { Qn = -Qn; Cd = -Cd; }     // the ideal of norm |Q'|
             Qd = Qn;
-            rQ = rcp64(Qd);
+            rQ = rcp64_1(Qd);
             // canonical P in (s - Q, s]: P_c = P' + k Q with k = floor((s - P')/Q)
             const double a = sd - Pn;
             double k = floor(a * rQ);
@@ -437,30 +433,9 @@ EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wm
             Cd = fma(-k, Pn + Pd, Cd);
             if (++nred > 4096) { *err += 1; break; }
         } while (Qd - Pd > sd);
+        t = mod3(t);
         dist += log2_approx((float)mag);
         if (fma(Qd, Cd, Pd * Pd) != (double)d) *err += 1;   // d = P^2 + Q C, exact (< 2^40)
-#else
-        // exact fp64 integers (|P|, Q < 2^32); Q' = (d - P'^2)/Q with d - P'^2 in int64
-        const double sd = (double)s;
-        double Qd = (double)Q, Pd = (double)P, rQ = rcp64(Qd);
-        do {
-            const double num = Pd + sd;
-            double q = floor(num * rQ);              // floor((P + sqrt d)/Q)
-            const double rr = fma(-q, Qd, num);
-            q = rr < 0.0 ? q - 1.0 : (rr >= Qd ? q + 1.0 : q);
-            const double Pn = fma(q, Qd, -Pd);
-            const i64 Pni = (i64)Pn;
-            const i64 nQ = d - Pni * Pni;
-            const double Qn = rint((double)nQ * rQ);
-            if ((i64)Qn * (i64)Qd != nQ) *err += 1;
-            t = mod3_small(t + 1u + (u32)((Pni >> 1) & 1));
-            dist += log2_approx((float)fabs(Pn + (double)g.sqrtd)) - log2_approx((float)Qd);
-            Qd = fabs(Qn);
-            rQ = rcp64(Qd);
-            Pd = sd - dfloor_mod(sd - Pn, Qd, rQ);   // canonical P in (s - Q, s]
-            if (++nred > 4096) { *err += 1; break; }
-        } while (Qd - Pd > sd);
-#endif
         Q = (i64)Qd;
         P = (i64)Pd;
     }
@@ -634,54 +609,28 @@ __device__ __forceinline__ void flush_stats(const WalkArgs &a, u64 baby, u64 gia
 // Shared memory per warp: the table (nb * BKT slots) and nb fill counters.
 EIS_HD u32 window_smem_words(u32 nb) { return nb * BKT + ((nb + 3) & ~3u); }
 
-// L2 policy of the window kernel (WIN_L2HINT bits): 2 = the build's list loads
-// evict_first (a list is dead in L2 once its store is built; the giant kernel
-// reads only the few entries a key match needs), 4 = the table write-out
-// evict_first (read only by the next kernel's probes).  With both, L2 keeps
-// more of the lists still waiting for their build: +3% on the bench line
-// (loads alone -0.6%, tables alone +0.8%; list stores evict_last -1.6%).
-// WIN_ST256: one 32-byte store (st.global.v8, sm_100) per 8 entries instead
-// of two 16-byte stores: +3.7%.
-#ifndef WIN_L2HINT
-#define WIN_L2HINT 6
-#endif
-#ifndef WIN_ST256
-#define WIN_ST256 1
-#endif
+// L2 policy of the window kernel: the build's list loads and the table write-out
+// are evict_first (a list is dead in L2 once its store is built -- the giant
+// kernel reads only the few entries a key match needs -- and a table is next
+// read by another kernel), so L2 keeps more of the lists still waiting for
+// their build: +3% on the bench line (loads alone -0.6%, tables alone +0.8%;
+// list stores evict_last -1.6%).
 __device__ __forceinline__ u64 l2_policy_first() {
     u64 p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 
+// one 32-byte store (st.global.v8, new on sm_100) per lane per 8 entries: one
+// whole sector per instruction (two 16-byte stores measured 3.7% slower)
 __device__ __forceinline__ void store_block(u32 *dst, const u32 (&e)[8]) {
-#if WIN_ST256
     asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                  ::"l"(dst), "r"(e[0]), "r"(e[1]), "r"(e[2]), "r"(e[3]), "r"(e[4]), "r"(e[5]),
                    "r"(e[6]), "r"(e[7]) : "memory");
-#else
-    reinterpret_cast<uint4 *>(dst)[0] = make_uint4(e[0], e[1], e[2], e[3]);
-    reinterpret_cast<uint4 *>(dst)[1] = make_uint4(e[4], e[5], e[6], e[7]);
-#endif
 }
 
-// a list group load of the build (16 bytes)
-__device__ __forceinline__ uint4 list_ld4(const uint4 *p) {
-#if (WIN_L2HINT & 2)
-    uint4 v;
-    asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_policy_first()));
-    return v;
-#else
-    return *p;
-#endif
-}
-
-// WIN_LD256: the build reads 8 entries per lane with one 32-byte load, which
-// also takes the evict_first priority as a plain qualifier (no createpolicy).
-#ifndef WIN_LD256
-#define WIN_LD256 1
-#endif
+// the build reads 8 entries per lane with one 32-byte load, which also takes the
+// evict_first priority as a plain qualifier (no createpolicy)
 __device__ __forceinline__ void list_ld8(const u32 *p, uint4 &a, uint4 &b) {
     asm volatile("ld.global.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
@@ -700,26 +649,13 @@ __device__ __forceinline__ void smem_st4_zero(u32 addr) {
     asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
 }
 
-#ifndef BUILD_K
-#define BUILD_K 2
-#endif
 // One store, built by the whole warp in shared memory (tab: nb * BKT slots, cnt:
-// nb fill counters, both zero on entry and on exit) and written to dst.
-__device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[BUILD_K]) {
+// nb fill counters, both zero on entry and on exit) and written to dst.  A
+// group is 256 entries, 8 per lane (two uint4 per lane).
+__device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[2]) {
     const int lane = threadIdx.x & 31;
-#if WIN_LD256
-    static_assert(BUILD_K == 2, "WIN_LD256 loads 8 entries per lane per group");
     nx[0] = nx[1] = make_uint4(0, 0, 0, 0);
     if (lst && 8u * (u32)lane < n) list_ld8(lst + 8 * lane, nx[0], nx[1]);
-#else
-    const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
-    const u32 n4 = (n + 3) >> 2;
-#pragma unroll
-    for (int k = 0; k < BUILD_K; k++) {
-        const u32 i4 = (u32)(32 * k + lane);
-        nx[k] = (lst && i4 < n4) ? list_ld4(l4 + i4) : make_uint4(0, 0, 0, 0);
-    }
-#endif
 }
 
 // nx: this d's first list group on entry (the caller or the previous call loaded
@@ -728,29 +664,17 @@ __device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[B
 // tab_s, cnt_s: shared-window addresses of the warp's table and counters.
 __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u32 *lst_next,
                                             u32 n, u32 nb, u32 tab_s, u32 cnt_s,
-                                            u32 *__restrict__ dst, uint4 (&nx)[BUILD_K]) {
+                                            u32 *__restrict__ dst, uint4 (&nx)[2]) {
     const int lane = threadIdx.x & 31;
-#if !WIN_LD256
-    const uint4 *l4 = reinterpret_cast<const uint4 *>(lst);
-    const u32 n4 = (n + 3) >> 2;
-#endif
-    constexpr int K = BUILD_K;                       // 16-byte loads per lane per group
+    constexpr int K = 2;                             // 16-byte halves per lane per group
     for (u32 jb = 0; jb < n; jb += 128 * K) {
         uint4 cur[K];
 #pragma unroll
         for (int k = 0; k < K; k++) cur[k] = nx[k];
         if (jb + 128 * K < n) {
-#if WIN_LD256
             const u32 j8 = jb + 128 * K + 8u * (u32)lane;
             nx[0] = nx[1] = make_uint4(0, 0, 0, 0);
             if (j8 < n) list_ld8(lst + j8, nx[0], nx[1]);
-#else
-#pragma unroll
-            for (int k = 0; k < K; k++) {
-                const u32 i4 = jb / 4 + (u32)(32 * K + 32 * k + lane);
-                nx[k] = i4 < n4 ? list_ld4(l4 + i4) : make_uint4(0, 0, 0, 0);
-            }
-#endif
         } else {
             load_group0(lst_next, n, nx);            // the next d's first group
         }
@@ -763,11 +687,7 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
 #pragma unroll
             for (int w = 0; w < 4; w++) {
                 const int i = 4 * k + w;
-#if WIN_LD256
                 const u32 j = jb + 8 * lane + 4 * k + w;
-#else
-                const u32 j = jb + 128 * k + 4 * lane + w;
-#endif
                 const u32 e = w == 0 ? cur[k].x : (w == 1 ? cur[k].y : (w == 2 ? cur[k].z : cur[k].w));
                 const u32 key = entry_key(e);
                 sv[i] = slot_entry(key, j);
@@ -802,13 +722,8 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) {
-#if (WIN_L2HINT & 4)
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
                      ::"l"(dst), "r"(tab_s), "r"(nb * BKT * 4u), "l"(l2_policy_first()) : "memory");
-#else
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                     ::"l"(dst), "r"(tab_s), "r"(nb * BKT * 4u) : "memory");
-#endif
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
@@ -889,7 +804,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             win++;
         }
         const u32 live = __ballot_sync(FULL_MASK, w.live);
-        uint4 nx[BUILD_K];
+        uint4 nx[2];
         if (live)
             load_group0(o.lists + (u64)(wave * 32 + (u32)(__ffs(live) - 1)) * B.lcap, (u32)B.nw, nx);
         for (u32 m = live; m; m &= m - 1) {
@@ -999,12 +914,6 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 // 4.1 M violations over C5; the paper's 50 is kept.)
 #define PLAIN_TH 50
 #endif
-#ifndef GIANT_DUP_FAST
-#define GIANT_DUP_FAST 0                      // 1: squarings in the giant kernel take nudupl_d
-#endif
-#ifndef GIANT_L2HINT
-#define GIANT_L2HINT 0                        // 1: table probes evict_first (-1%)
-#endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
 bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
@@ -1087,17 +996,11 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 const u32 dst = (u32)__cvta_generic_to_shared(&pbuf[threadIdx.x][0]);
 #pragma unroll
                 for (int q = 0; q < 4; q++)
-#if GIANT_L2HINT
-                    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-                                 ::"r"(dst + 16 * q), "l"(src + 4 * q), "l"(l2_policy_first())
-                                 : "memory");
-#else
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q),
                                  "l"(src + 4 * q) : "memory");
-#endif
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
-            const GiantInfo gi = giant_advance(g, B, &err, gmask, GIANT_DUP_FAST != 0);
+            const GiantInfo gi = giant_advance(g, B, &err, gmask, false);
             giant++;
             red += gi.nred;
             asm volatile("cp.async.wait_group 0;" ::: "memory");

@@ -185,3 +185,23 @@ def test_table1_prefix_total():
     cD, cE = C.count_window(lo, [hi])
     assert int(cE[0]) == want
     assert int(cD[0]) == pi_D_closed_form(hi)
+
+
+def test_count_window_boundaries_at_candidates():
+    """eo_count_window at x = 5 (mod 8) (PAPER.md l.105-108: d <= x inclusive;
+    windows exclude lo): 5 is the least d in D (t = 1, not in E) and 37 the
+    least d in E (eps = 6 + sqrt 37); pi_D by the Moebius closed
+    form at candidate-valued checkpoints and window ends."""
+    cD, cE = C.count_window(0, [5, 37])
+    assert list(cD) == [1, 5] and list(cE) == [0, 1]
+    cD, cE = C.count_window(5, [37])                  # (5, 37]: 13, 21, 29, 37
+    assert list(cD) == [4] and list(cE) == [1]
+    cD, cE = C.count_window(37, [45])                 # (37, 45]: 45 = 9 * 5 is not in D
+    assert list(cD) == [0] and list(cE) == [0]
+    xs = [10_005, 99_997, 123_461, 200_005]            # all = 5 (mod 8)
+    assert all(x % 8 == 5 for x in xs)
+    cD, _ = C.count_window(0, xs)
+    assert [int(v) for v in cD] == [pi_D_closed_form(x) for x in xs]
+    lo = 10_005
+    cD, _ = C.count_window(lo, xs[1:])
+    assert [int(v) for v in cD] == [pi_D_closed_form(x) - pi_D_closed_form(lo) for x in xs[1:]]
