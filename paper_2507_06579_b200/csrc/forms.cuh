@@ -179,6 +179,8 @@ struct Composed {
     u32 tg;        // t(gamma) in {0,1,2}
     float lg;      // log2 |gamma|
     u32 kind;      // 0 plain product, 1 NUCOMP, 2 NUDUPL
+    u32 nerr;      // invariant violations (returned, not through a pointer: the out-of-line
+                   // caller's counter then stays in a register)
 };
 
 // residue of gamma from the final Euclid cofactors (R12)
@@ -387,11 +389,16 @@ EIS_HD Mu1Form mu1_form(i64 Q1, i64 P1, i64 d, u32 *err) {
 
 // Algorithm 4 NUCOMPchoose for reduced ideals
 // I1 = mu_1 = [Q1/2, (P1+sqrt d)/2] (pre-normalised) and I2 = [Q2/2, (P2+sqrt d)/2].
-EIS_HD_COLD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 L, double sqrtd,
-                              int plain_th, u32 *err) {
+EIS_HD_COLD Composed nucomp_choose(Mu1Form m1, i64 Q2, i64 P2, i64 d, i64 L, double sqrtd,
+                                   int plain_th) {
+    u32 nerr = 0, *err = &nerr;
     const i64 Q1 = m1.Q, P1 = m1.P;
     P2 = P2 < Q2 ? P2 : floor_mod(P2, Q2);
-    if (Q1 <= plain_th || Q2 <= plain_th) return plain_product(Q1, P1, Q2, P2, d, err);
+    if (Q1 <= plain_th || Q2 <= plain_th) {
+        Composed r = plain_product(Q1, P1, Q2, P2, d, err);
+        r.nerr = nerr;
+        return r;
+    }
     i64 u3, v3, w3, G, x, y;
     Composed r;
     if (Q1 == Q2 && P1 == P2) {
@@ -409,6 +416,7 @@ EIS_HD_COLD Composed nucomp_choose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64
     r.tg = t_gamma(x, y, v3);
     r.lg = log2_gamma(G, x, y, u3, v3, (float)sqrtd, Q1, Q2);
     if ((r.Q & 3) != 2 || (r.P & 1) != 1 || (G & 1) == 0) *err += 1;   // Thm A.1 / 2 inert
+    r.nerr = nerr;
     return r;
 }
 
@@ -614,7 +622,8 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     const u32 dmask = dup_fast ? warp_ballot(wmask, fdup) : 0u;
     if (rare) {
         EIS_PROF(8);
-        const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
+        const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th);
+        *err += c.nerr;
         r.Q = c.Q;
         r.P = s - floor_mod(s - c.P, c.Q);
         r.tg = c.tg;
@@ -633,7 +642,8 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
                       -(double)P2, w2, (float)L, o, err, fmask);
     }
     if (!ok) {
-        const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th, err);
+        const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th);
+        *err += c.nerr;
         r.Q = c.Q;
         r.P = s - floor_mod(s - c.P, c.Q);
         r.tg = c.tg;

@@ -96,9 +96,14 @@ EIS_HD float two_sided_margin2(u64 d) {            // M in log2 units
 }
 
 // ---------------------------------------------------------------- the store --
-EIS_HD u32 list_entry(u32 Q, u32 traw) { return Q | (traw << 20); }
+// list entry = key | t << 18 with key = Q >> 2 = (Q - 2)/4 (Q = 2 mod 4 on reduced
+// ideals; Q < 2^20 so key < 2^18) and t the unreduced residue count (< 2^14)
+EIS_HD u32 list_entry(u32 Q, u32 traw) { return (Q >> 2) | (traw << 18); }
+EIS_HD u32 list_entry_key(u32 key, u32 traw) { return key | (traw << 18); }
+EIS_HD u32 entry_Q(u32 e) { return 4u * (e & 0x3FFFFu) + 2u; }
+EIS_HD u32 entry_t(u32 e) { return e >> 18; }
 // key = Q >> 2 identifies Q (Q = 2 mod 4 on reduced ideals)
-EIS_HD u32 entry_key(u32 e) { return (e & 0xFFFFFu) >> 2; }
+EIS_HD u32 entry_key(u32 e) { return e & 0x3FFFFu; }
 EIS_HD u32 slot_entry(u32 key, u32 j) { return key | ((j + 1) << 18); }
 EIS_HD u32 store_bucket(u32 key, u32 nb) {         // multiply-shift hash onto [0, nb)
 #ifdef __CUDA_ARCH__
@@ -178,7 +183,7 @@ EIS_HD u32 bucket_slot(const Probe &p, int i) {      // i: compile-time after un
 }
 
 // Slots before the first empty one (all 16 if the bucket is full).
-EIS_HD_COLD u32 filled_mask(const Probe &p) {
+EIS_HD u32 filled_mask(const Probe &p) {
     u32 em = 0;
 #pragma unroll
     for (int i = 0; i < BKT; i++) em |= (u32)(bucket_slot(p, i) == 0) << i;
@@ -191,8 +196,10 @@ EIS_HD_COLD u32 filled_mask(const Probe &p) {
 // per bucket in the build), so it is full iff its last slot is, and an empty slot
 // (0) can match only key 0 (Q = 2), which masks the empty slots off (rare).  A
 // key match (about one per d) re-reads its slot and checks P (R34, R35).
+// first_slots (nullable): a copy of the first probed bucket (the giant kernel's
+// shared-memory buffer), read on a key match instead of global memory.
 EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d, u32 s,
-                         u32 Q, u32 P, u32 &t3, u32 &j) {
+                         u32 Q, u32 P, u32 &t3, u32 &j, const u32 *first_slots = nullptr) {
     const u32 qk = Q >> 2;
     for (;;) {
         u32 mm = 0;
@@ -205,12 +212,12 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
             EIS_PROF(9);
             const int i = __builtin_ctz_portable(mm);
             mm &= mm - 1;
-            const u32 e = tab[(size_t)p.b * BKT + i];
+            const u32 e = first_slots ? first_slots[i] : tab[(size_t)p.b * BKT + i];
             const u32 jj = ((e >> 18) & 0x7FFu) - 1;
-            const u32 Qprev = jj ? (list[jj - 1] & 0xFFFFFu) : 0u;
+            const u32 Qprev = jj ? entry_Q(list[jj - 1]) : 0u;
             const int k = match_kind(d, Q, P, s, jj, Qprev);
             if (k != HIT_NONE) {
-                t3 = jj ? mod3(list[jj] >> 20) : 0u;      // t(theta), from the list
+                t3 = jj ? mod3(entry_t(list[jj])) : 0u;   // t(theta), from the list
                 j = jj;
                 return k;
             }
@@ -218,6 +225,7 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
         if (!full) return HIT_NONE;
         EIS_PROF(10);
         load_bucket(tab, next_bucket(p.b, nb), p);       // bucket full: continue
+        first_slots = nullptr;
     }
 }
 
@@ -243,6 +251,8 @@ EIS_HD bool baby_step_fd(BabyStateF &st, float sqd_m, float &prod) {
 }
 
 EIS_HD u32 f_to_u(float v) { return f2u_bits(v + 8388608.0f) - 0x4B000000u; }   // v < 2^23
+// key = (Q - 2)/4 of an exact float Q = 2 mod 4: Q/4 + (2^23 - 1/2) = key + 2^23 exactly
+EIS_HD u32 f_to_key(float Q) { return f2u_bits(fmaf(Q, 0.25f, 8388607.5f)) - 0x4B000000u; }
 
 
 struct WinLane {
@@ -310,7 +320,7 @@ EIS_HD u32 win_step(WinLane &w) {
         w.res = baby_result_f(w.st);
         w.live = false;
     }
-    return list_entry(f_to_u(w.st.Q), w.st.t2 >> 1);
+    return list_entry_key(f_to_key(w.st.Q), w.st.t2 >> 1);
 }
 
 // fold the pending multipliers into the distance (every 4 steps: entry j = 3 mod 4)
@@ -553,17 +563,26 @@ EIS_HD void giant_unpack(GiantLane &g, const GiantRec &r, u64 d) {
 }
 
 // exact half walk for one d (guard inconclusive / cap exceeded)
-EIS_HD_COLD u32 half_walk_one(u64 d, u64 &steps, u32 &err) {
+// (results returned by value, not through references: the out-of-line call then
+// does not force the caller's counters into local memory)
+struct HalfOne {
+    u32 res, err, steps;
+};
+EIS_HD_COLD HalfOne half_walk_one(u64 d) {
+    HalfOne h{0, 0, 0};
     BabyState st;
     u32 r1;
-    if (baby_init(st, d, &r1)) return r1;
+    if (baby_init(st, d, &r1)) {
+        h.res = r1;
+        return h;
+    }
     const u32 cap = half_step_cap(st.s);
     u32 j = 0;
     bool ok;
-    do { steps++; ok = baby_step(st); } while (!ok && ++j <= cap);
-    if (ok) return baby_result(st);
-    err++;
-    return 0xFFu;
+    do { h.steps++; ok = baby_step(st); } while (!ok && ++j <= cap);
+    if (ok) h.res = baby_result(st);
+    else { h.err = 1; h.res = 0xFFu; }
+    return h;
 }
 
 // ------------------------------------------------------------------ kernels --
@@ -682,17 +701,18 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
         // full buckets (rare)
         u32 ovf = 0;                                     // bit i: entry i still to place
         u32 bb[4 * K], sv[4 * K];
+        // n is a multiple of 8, so a lane's 8 entries are all in the list or all past it
+        if (jb + 8 * (u32)lane < n) {
 #pragma unroll
-        for (int k = 0; k < K; k++) {
+            for (int k = 0; k < K; k++) {
 #pragma unroll
-            for (int w = 0; w < 4; w++) {
-                const int i = 4 * k + w;
-                const u32 j = jb + 8 * lane + 4 * k + w;
-                const u32 e = w == 0 ? cur[k].x : (w == 1 ? cur[k].y : (w == 2 ? cur[k].z : cur[k].w));
-                const u32 key = entry_key(e);
-                sv[i] = slot_entry(key, j);
-                bb[i] = store_bucket(key, nb);
-                if (j < n) {
+                for (int w = 0; w < 4; w++) {
+                    const int i = 4 * k + w;
+                    const u32 j = jb + 8 * lane + 4 * k + w;
+                    const u32 e = w == 0 ? cur[k].x : (w == 1 ? cur[k].y : (w == 2 ? cur[k].z : cur[k].w));
+                    const u32 key = entry_key(e);
+                    sv[i] = slot_entry(key, j);
+                    bb[i] = store_bucket(key, nb);
                     const u32 pos = smem_atom_inc(cnt_s + 4 * bb[i]);
                     if (pos < (u32)BKT) smem_st(tab_s + 4 * (bb[i] * BKT + pos), sv[i]);
                     else ovf |= 1u << i;
@@ -879,7 +899,10 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         }
         if (g.phase == PH_HALF) {                              // inconclusive guard (tiny d)
             fb++;
-            g.res = half_walk_one(g.d, baby, err);
+            const HalfOne h = half_walk_one(g.d);
+            g.res = h.res;
+            baby += h.steps;
+            err += h.err;
             g.phase = PH_DONE;
         }
         if (g.phase == PH_DONE) {
@@ -1011,7 +1034,8 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             pr.g2 = pbuf[threadIdx.x][2];
             pr.g3 = pbuf[threadIdx.x][3];
             u32 te, j;
-            const int kind = store_resolve(tab, list, B.nb, pr, g.d, (u32)g.s, pQ, pP, te, j);
+            const int kind = store_resolve(tab, list, B.nb, pr, g.d, (u32)g.s, pQ, pP, te, j,
+                                           reinterpret_cast<const u32 *>(&pbuf[threadIdx.x][0]));
             warp_reconverge(gmask);
             if (kind != HIT_NONE) {
                 g.phase = giant_hit(g, kind, te, pt, pdist, pQ, g.res) ? PH_DONE : PH_HALF;
@@ -1020,7 +1044,10 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             }
             if (g.phase == PH_HALF) {     // exact half walk instead
                 fb++;
-                g.res = half_walk_one(g.d, baby, err);
+                const HalfOne h = half_walk_one(g.d);
+            g.res = h.res;
+            baby += h.steps;
+            err += h.err;
                 g.phase = PH_DONE;
             }
         }

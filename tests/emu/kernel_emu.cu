@@ -119,7 +119,10 @@ int main(int argc, char **argv) {
                     }
                     if (g.phase == PH_HALF) {
                         fb++;
-                        g.res = half_walk_one(d, baby, err);
+                        const HalfOne h = half_walk_one(d);
+                        g.res = h.res;
+                        baby += h.steps;
+                        err += h.err;
                     }
                     res = g.res;
                 }
