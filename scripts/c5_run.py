@@ -7,7 +7,7 @@ Moebius closed form; fits
   eq. (pdata) pi_{E cap P}(x) ~ pi(x)/12 + a int_2^x dt/(t^(1/6) ln t)
             (l.503-507, a ~ -0.037), with pi(x)/12 ~ pi_{D cap P}(x)/3
             (primes = 5 mod 8 are pi(x)/4 up to lower-order terms).
-Writes profiles/r01_c5_checkpoints.csv and prints a JSON summary."""
+Writes profiles/$EIS_TAG_c5_checkpoints.csv (EIS_TAG, default r02) and prints a JSON summary."""
 import json, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -24,7 +24,7 @@ t0 = time.time()
 R = eis.count_window_ext(0, x)
 wall = time.time() - t0
 st = eis.get_stats()
-out = os.path.join(ROOT, "profiles", "r01_c5_checkpoints.csv")
+out = os.path.join(ROOT, "profiles", os.environ.get("EIS_TAG", "r02") + "_c5_checkpoints.csv")
 with open(out, "w") as f:
     f.write("x,pi_D,pi_E,pi_T1,pi_DP,pi_EP\n")
     for i, a in enumerate(x):

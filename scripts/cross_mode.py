@@ -24,4 +24,4 @@ for lo, hi in [(9 * 10**9, 10**10), (10**11 - 10**9, 10**11)]:
     print(json.dumps(res), flush=True)
 eis.set_option("mode", eis.MODE_AUTO)
 json.dump(out, open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                 "profiles", "r01_cross_mode.json"), "w"), indent=1)
+                                 "profiles", os.environ.get("EIS_TAG", "r02") + "_cross_mode.json"), "w"), indent=1)
