@@ -387,75 +387,106 @@ struct GiantInfo {
     u32 nred;       // rho steps in the reduction
 };
 
+// The rho reduction of a giant step's output (R18, R28), in exact fp64
+// integers, carrying the third coefficient C = (d - P^2)/Q of the ideal (Q, P)
+// so that no step forms d - P'^2 (|P'| reaches 2^28, so that needs int64):
+// rho gives P' = qQ - P, Q' = C + q (P - P'), C' = Q, and moving P' to its
+// canonical representative P' + kQ' gives C' - k (P' + P'_c).  Every result
+// is an integer below 2^38 and each product is inside an fma (one rounding of
+// an exact value), so all of it is exact even where k (P' + P'_c) itself
+// exceeds 2^53.  The residue bit of P' is read from the low word of
+// P' + 1.5 * 2^52 (no conversion), and the distance is accumulated as a
+// product, with one log at the end.  (A resumable form, at most 1-3 steps per
+// warp iteration with the rest parked in shared memory, measured 1.8-2.8%
+// slower than running each lane's loop to the end: DESIGN.md 4, dead ends.)
+struct RhoState {
+    double Q, P, C, rQ, mag;   // the current ideal, 1/Q, prod |P' + sqrt d| / Q
+    u32 t;                     // t(mu) (not reduced mod 3 while stepping)
+    u32 nred;                  // rho steps so far
+    float dist;                // log2 of the generator, without mag
+};
+
+// The output of a composition: rho state with Q, P canonical (P in (s - Q, s]).
+EIS_HD RhoState rho_begin(const GiantLane &g, const GiantComp &c) {
+    RhoState r;
+    r.t = mod3_small(g.t1 + g.tc + 3u - c.tg);   // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
+    r.dist = g.dist1 + g.distc - c.lg;
+    r.Q = (double)c.Q;
+    r.P = (double)c.P;
+    r.nred = 0;
+    r.mag = 1.0;
+    r.rQ = 0.0;
+    r.C = 0.0;
+    if (c.Q - c.P > (i64)g.s) {                  // not reduced: C = (d - P^2)/Q
+        // |P| < Q + s may reach 2^28, so d - P^2 in int64; the quotient is < 2^37
+        // and the division exact, so rint recovers it
+        r.rQ = rcp64_1(r.Q);
+        r.C = rint((double)((i64)g.d - c.P * c.P) * r.rQ);
+    }
+    return r;
+}
+
+EIS_HD bool rho_needed(const RhoState &r, double sd) { return r.Q - r.P > sd; }
+
+// one rho step plus the canonical shift
+EIS_HD void rho_step(RhoState &r, double sd, double sqrtd) {
+    EIS_PROF(3);
+    const double num = r.P + sd;
+    double q = floor(num * r.rQ);                // floor((P + sqrt d)/Q)
+    const double rr = fma(-q, r.Q, num);
+    q = rr < 0.0 ? q - 1.0 : (rr >= r.Q ? q + 1.0 : q);
+    const double Pn = fma(q, r.Q, -r.P);
+    double Qn = fma(q, r.P - Pn, r.C);
+    const u32 plo = (u32)__double2loint_hd(Pn + 6755399441055744.0);   // P' mod 2^32
+    r.t += 1u + ((plo >> 1) & 1u);               // (reduced mod 3 at rho_end)
+    r.mag *= fabs(Pn + sqrtd) * r.rQ;
+    double Cn = r.Q;                             // C' = Q
+    if (Qn < 0.0) { Qn = -Qn; Cn = -Cn; }        // the ideal of norm |Q'|
+    r.Q = Qn;
+    r.rQ = rcp64_1(Qn);
+    // canonical P in (s - Q, s]: P_c = P' + k Q with k = floor((s - P')/Q)
+    const double a = sd - Pn;
+    double k = floor(a * r.rQ);
+    const double rk = fma(-k, Qn, a);
+    k = rk < 0.0 ? k - 1.0 : (rk >= Qn ? k + 1.0 : k);
+    r.P = fma(k, Qn, Pn);
+    r.C = fma(-k, Pn + r.P, Cn);
+    r.nred++;
+}
+
+// mu'_k = the reduced result: residue, distance, the exact check d = P^2 + Q C
+EIS_HD void rho_end(GiantLane &g, RhoState &r, u32 *err) {
+    if (r.nred) {
+        r.t = mod3(r.t);
+        r.dist += log2_approx((float)r.mag);
+        if (fma(r.Q, r.C, r.P * r.P) != (double)g.d) *err += 1;   // exact (< 2^40)
+    }
+    g.k++;
+    g.Qc = (u32)r.Q;
+    g.Pc = (u32)r.P;
+    g.tc = r.t;
+    g.distc = r.dist;
+}
+
 // Advance: mu'_k = rho-reduce(NUCOMPchoose(mu_1, mu'_{k-1})) with its residue and
 // distance; no lookup.  *err counts invariant violations.
 // dup_fast: the step is (normally) a squaring, mu'_k = mu_1^2 (the prep kernel)
 EIS_HD GiantInfo giant_advance(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmask = 0xffffffffu,
                                bool dup_fast = false) {
     GiantInfo gi;
-    const i64 d = (i64)g.d;
-    const i64 s = g.s;
-    const GiantComp c = giant_compose(g.m1, (i64)g.Qc, (i64)g.Pc, d, s, (i64)g.L, g.sqrtd,
-                                      B.plain_th, err, wmask, dup_fast);
+    const GiantComp c = giant_compose(g.m1, (i64)g.Qc, (i64)g.Pc, (i64)g.d, (i64)g.s, (i64)g.L,
+                                      g.sqrtd, B.plain_th, err, wmask, dup_fast);
     warp_reconverge(wmask);
     gi.kind = c.kind;
-    u32 t = mod3_small(g.t1 + g.tc + 3u - c.tg);   // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
-    float dist = g.dist1 + g.distc - c.lg;
-    i64 Q = c.Q, P = c.P;                        // P canonical in (s - Q, s]
-    u32 nred = 0;
-    if (Q - P > s) {                             // not reduced (R18): apply rho
-        // Exact fp64 integers, carrying the third coefficient C = (d - P^2)/Q of
-        // the ideal (Q, P) so that no step forms d - P'^2 (|P'| reaches 2^28, so
-        // that needs int64): rho gives P' = qQ - P, Q' = C + q (P - P'), C' = Q,
-        // and moving P' to its canonical representative P' + kQ' gives
-        // C' - k (P' + P'_c).  Every result is an integer below 2^38 and each
-        // product is inside an fma (one rounding of an exact value), so all
-        // of it is exact even where k (P' + P'_c) itself exceeds 2^53.  The residue bit
-        // of P' is read from the low word of P' + 1.5 * 2^52 (no conversion), and
-        // the distance is accumulated as a product, with one log at the end.
-        const double sd = (double)s;
-        double Qd = (double)Q, Pd = (double)P, rQ = rcp64_1(Qd);
-        // C = (d - P^2)/Q: |P| < Q + s may reach 2^28, so d - P^2 in int64; the
-        // quotient is < 2^37 and the division exact, so rint recovers it
-        double Cd = rint((double)(d - P * P) * rQ);
-        double mag = 1.0;                               // prod |P' + sqrt d| / Q
-        do {
-            EIS_PROF(3);
-            const double num = Pd + sd;
-            double q = floor(num * rQ);              // floor((P + sqrt d)/Q)
-            const double rr = fma(-q, Qd, num);
-            q = rr < 0.0 ? q - 1.0 : (rr >= Qd ? q + 1.0 : q);
-            const double Pn = fma(q, Qd, -Pd);
-            double Qn = fma(q, Pd - Pn, Cd);
-            const u32 plo = (u32)__double2loint_hd(Pn + 6755399441055744.0);   // P' mod 2^32
-            t += 1u + ((plo >> 1) & 1u);             // (reduced mod 3 after the loop)
-            mag *= fabs(Pn + (double)g.sqrtd) * rQ;
-            Cd = Qd;                                  // C' = Q
-            if (Qn < 0.0) { Qn = -Qn; Cd = -Cd; }     // the ideal of norm |Q'|
-            Qd = Qn;
-            rQ = rcp64_1(Qd);
-            // canonical P in (s - Q, s]: P_c = P' + k Q with k = floor((s - P')/Q)
-            const double a = sd - Pn;
-            double k = floor(a * rQ);
-            const double r = fma(-k, Qd, a);
-            k = r < 0.0 ? k - 1.0 : (r >= Qd ? k + 1.0 : k);
-            Pd = fma(k, Qd, Pn);
-            Cd = fma(-k, Pn + Pd, Cd);
-            if (++nred > 4096) { *err += 1; break; }
-        } while (Qd - Pd > sd);
-        t = mod3(t);
-        dist += log2_approx((float)mag);
-        if (fma(Qd, Cd, Pd * Pd) != (double)d) *err += 1;   // d = P^2 + Q C, exact (< 2^40)
-        Q = (i64)Qd;
-        P = (i64)Pd;
+    RhoState r = rho_begin(g, c);
+    const double sd = (double)g.s;
+    while (rho_needed(r, sd)) {
+        rho_step(r, sd, (double)g.sqrtd);
+        if (r.nred > 4096) { *err += 1; break; }
     }
     warp_reconverge(wmask);
-    gi.nred = nred;
-    g.k++;
-    g.Qc = (u32)Q;
-    g.Pc = (u32)P;
-    g.tc = t;
-    g.distc = dist;
+    gi.nred = r.nred;
+    rho_end(g, r, err);
     return gi;
 }
 
@@ -1007,8 +1038,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             const u32 *tab = o.tables + (u64)gidx * ((u64)B.nb * BKT);
             const u32 *list = o.lists + (u64)gidx * B.lcap;
             // software pipeline: probe mu'_k (refills start with mu'_2, not yet
-            // probed) while computing mu'_{k+1}
-            // probed while computing mu'_{k+1}; the bucket is copied to shared
+            // probed) while computing mu'_{k+1}; the bucket is copied to shared
             // memory asynchronously (cp.async), so no registers wait across the
             // composition and the compiler cannot sink the load to its use
             const u32 pQ = g.Qc, pP = g.Pc, pt = g.tc;
