@@ -432,9 +432,13 @@ def main():
             per_kernel["half"] = {"ms": kms["window"]}
             ops = 14 * stats["baby_steps"]
             a_t = ops / (kms["window"] / 1e3) / 1e12
+            meas = kc.get("walk_half_kernel", {}).get("thread_inst_per_baby_step")
             roofline = {"bound": "issue", "kernel": "walk_half_kernel", "achieved": a_t,
                         "peak": issue_peak_tops, "unit": "T thread-ops/s", "frac": a_t / issue_peak_tops,
-                        "traffic": None, "basis": "14 thread-instructions per rho step (DESIGN.md 4)"}
+                        "traffic": None,
+                        "basis": f"14 thread-instructions per rho step (the step's SASS, DESIGN.md 4; "
+                                 f"ncu measures {meas and round(meas, 1)} per step with loop and "
+                                 f"refill overhead, {UNIT_COUNTS})"}
         roofline["per_kernel"] = per_kernel
         roofline["walk_ms_per_step"] = kms["walk"]
         roofline["walk_share_of_step"] = kms["walk"] / (tot_ms_max / args.steps)

@@ -36,7 +36,14 @@ def run() -> None:
     eis.init(0)
     D, E = eis.count_window(lo, [hi])
     st = eis.get_stats()
-    out = {"lo": lo, "hi": hi, "D": int(D[0]), "E": int(E[0]), **st}
+    # the HALF walk's per-step count, on (9.9e8, 1e9] (AUTO's HALF region)
+    eis.set_option("mode", eis.MODE_HALF)
+    eis.count_window(990_000_000, [1_000_000_000])
+    sh = eis.get_stats()
+    eis.set_option("mode", eis.MODE_AUTO)
+    out = {"lo": lo, "hi": hi, "D": int(D[0]), "E": int(E[0]), **st,
+           "half": {"lo": 990_000_000, "hi": 1_000_000_000, "d": sh["d_classified"],
+                    "baby_steps": sh["baby_steps"]}}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "unit_stats.json"), "w") as f:
         json.dump(out, f)
@@ -51,8 +58,18 @@ def combine(csv_path: str, stats_path: str, out_path: str) -> None:
     kern = collections.defaultdict(lambda: collections.defaultdict(float))
     launches = collections.Counter()
     seen = set()
+    second_call, prefix_id = False, None
     for r in rows[1:]:
         name = r[k].split("(")[0].split("::")[-1].replace("<unnamed>", "").strip()
+        name = name[5:] if name.startswith("void ") else name
+        if prefix_id is not None and r[h.index("ID")] != prefix_id:
+            second_call = True                 # past the first call's prefix kernel
+        if name.startswith("walk_half_kernel"):
+            name = "walk_half_kernel"
+        elif second_call:                      # kernels of the HALF call
+            name += " (HALF call)"
+        elif name.startswith("prefix_kernel"):
+            prefix_id = r[h.index("ID")]
         kern[name][r[m]] += float(r[v].replace(",", ""))
         if (r[h.index("ID")], name) not in seen:
             seen.add((r[h.index("ID")], name))
@@ -61,7 +78,7 @@ def combine(csv_path: str, stats_path: str, out_path: str) -> None:
     out = {"source": "ncu --metrics (counters summed over the call's launches) of one "
                      f"count_window({st['lo']}, [{st['hi']}]) call; stats from eis_get_stats",
            "d": nd, "baby_steps": st["baby_steps"], "giant_steps": st["giant_steps"],
-           "reduce_steps": st["reduce_steps"], "kernels": {}}
+           "reduce_steps": st["reduce_steps"], "half_call": st.get("half"), "kernels": {}}
     pipes = ("alu", "fma", "fmaheavy", "fp64", "xu", "lsu", "uniform", "cbu", "adu")
     for name, d in kern.items():
         w = d["smsp__inst_executed.sum"]
@@ -78,6 +95,14 @@ def combine(csv_path: str, stats_path: str, out_path: str) -> None:
             e["thread_inst_per_baby_step"] = e["thread_inst"] / st["baby_steps"]
         if name == "bsgs_giant_kernel":
             e["thread_inst_per_giant_step"] = e["thread_inst"] / st["giant_steps"]
+        if name.startswith("walk_half_kernel") and st.get("half"):
+            e["thread_inst_per_baby_step"] = e["thread_inst"] / st["half"]["baby_steps"]
+            for key in ("warp_inst_per_d", "thread_inst_per_d", "dram_bytes_per_d",
+                        "dram_read_per_d", "dram_write_per_d"):
+                e[key] = e[key] * nd / st["half"]["d"]
+            e["pipe_warp_inst_per_d"] = {p: v * nd / st["half"]["d"]
+                                         for p, v in e["pipe_warp_inst_per_d"].items()}
+            e["per_d_basis"] = "d of the HALF call"
         out["kernels"][name] = e
     json.dump(out, open(out_path, "w"), indent=1)
     print(json.dumps({n: {kk: e[kk] for kk in ("warp_inst_per_d", "thread_inst_per_d",
