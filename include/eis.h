@@ -100,7 +100,8 @@ EIS_API const char *eis_last_error(void);
  *  "blocks_per_sm" HALF walk kernel CTAs per SM
  *  "giant_ctas"    BSGS giant kernel CTAs per SM (0 = occupancy maximum)
  *  "window_ctas"   BSGS window kernel CTAs per SM (0 = occupancy maximum)
- *  "bsgs_gb"       BSGS store memory per segment buffer in GiB (two buffers), [1, 64]
+ *  "bsgs_gb"       BSGS store memory per segment buffer in GiB, [1, 160], default 48: two
+ *                  buffers; a range whose stores fit in 2 bsgs_gb GiB runs as one segment
  *  "giant_cap"     BSGS giant steps per d before the exact half walk takes over:
  *                  giant_cap * (d^(1/4) + 10), in [0, 1000] (default 20; 0 sends
  *                  every d past k = 2 to the half walk, a test of that path)

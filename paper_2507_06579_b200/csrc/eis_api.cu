@@ -77,8 +77,8 @@ struct Ctx {
     int window_ctas = 0;             // BSGS window kernel CTAs per SM (0 = occupancy maximum)
     int giant_cap = 20;              // BSGS giant steps per d before the exact half walk takes
                                      // over: giant_cap * (d^(1/4) + 10) (tests force it to 0)
-    int bsgs_gb = 48;                // BSGS store memory per segment buffer (two buffers): fewer
-                                     // segments, fewer giant-kernel tails (32 -> 48: +1.2% at 1e10)
+    int bsgs_gb = 48;                // BSGS store memory per segment buffer in GiB (two buffers;
+                                     // a range within 2 bsgs_gb GiB runs as one segment)
     int half_ksteps = 0;             // 0: chosen per segment from d
     int two_sided = 1;               // BSGS: two-sided window (R35); 0 = paper's Alg. 1
     // instrumentation of the last call
@@ -297,14 +297,21 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     const u64 SEG = 1ull << g.segment_log2;
     const int n_small = primes_small();
     const int n_small1 = primes_upto_sq((u64)SIEVE_CHUNK * SIEVE_CHUNK / (64 * 64));   // p <= chunk/64
-    // BSGS keeps one store per survivor of the segment (two segment buffers):
-    // cap the segment so the stores stay within bsgs_gb GiB of HBM per buffer.
+    // BSGS keeps one store per candidate slot of the segment, in two segment
+    // buffers of at most bsgs_gb GiB each -- or, when the whole range fits in
+    // 2 bsgs_gb GiB, as ONE segment in one buffer: fewer segments, fewer
+    // giant-kernel tails (the bench slab as one segment instead of two measured
+    // +1.5%, Layout).
     const bool bsgs = want_bsgs(cand_d(i_first));
     u64 seg_cap = SEG;
     if (bsgs) {
         const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), alpha_for(cand_d(i_last)) / 16.0f,
                                                 g.two_sided);
-        seg_cap = std::min<u64>(SEG, std::max<u64>(((u64)g.bsgs_gb << 30) / per, 1ull << 16));
+        const u64 total = i_last - i_first + 1;
+        const u64 cap_bytes = (u64)g.bsgs_gb << 30;
+        seg_cap = total * per <= 2 * cap_bytes ? total
+                                               : std::max<u64>(cap_bytes / per, 1ull << 16);
+        seg_cap = std::min<u64>(SEG, seg_cap);
     }
     // equal segments: a short remainder segment would be all giant-kernel tail
     {
@@ -324,7 +331,10 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         // (results do not depend on it) down to 2^16 candidates
         for (;;) {
             bool ok = true;
-            for (SegBuf &b : g.buf) {
+            // a range of one segment needs one buffer (the other may be freed to make room)
+            const int nbuf = i_last - i_first + 1 > seg_cap ? 2 : 1;   // one segment: one buffer
+            for (int ib = 0; ib < nbuf; ib++) {
+                SegBuf &b = g.buf[ib];
                 if (b.bsgs.lists && b.bsgs.lists_n >= seg_cap * (size_t)lcap &&
                     b.bsgs.tables_n >= seg_cap * (size_t)nbk * BKT && b.bsgs.brecs_n >= seg_cap)
                     continue;
@@ -761,7 +771,7 @@ int eis_set_option(const char *key, int64_t v) {
         if (v < 0 || v > 1000) return fail(EIS_EINVAL, "giant_cap must be in [0, 1000]");
         g.giant_cap = (int)v;
     } else if (k == "bsgs_gb") {
-        if (v < 1 || v > 64) return fail(EIS_EINVAL, "bsgs_gb must be in [1, 64]");
+        if (v < 1 || v > 160) return fail(EIS_EINVAL, "bsgs_gb must be in [1, 160]");
         g.bsgs_gb = (int)v;
     } else if (k == "window_ctas") {
         if (v < 0 || v > 32) return fail(EIS_EINVAL, "window_ctas must be in [0, 32]");

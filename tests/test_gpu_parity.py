@@ -364,6 +364,9 @@ def test_bsgs_scratch_shrinks_under_memory_pressure():
             hold = torch.empty(free - keep, dtype=torch.uint8, device="cuda:0")
         D, E = eis.count_window(9_900_000_000, [10_000_000_000])
         assert int(E[0]) == 3_334_227
+        eis.set_option("bsgs_gb", 96)             # one segment requested: halved as needed
+        D2, E2 = eis.count_window(9_900_000_000, [10_000_000_000])
+        assert int(E2[0]) == 3_334_227 and int(D2[0]) == int(D[0])
     finally:
         del hold
         torch.cuda.empty_cache()
