@@ -39,9 +39,16 @@ EIS_HD double rcp64(double b) {
 #endif
 }
 
-// 1/b with one Newton step from the MUFU.RCP64H seed (relative error ~2^-40):
-// enough wherever a floor or rint of n * r is corrected by one exact remainder
-// test or the quotient stays below ~2^38 (the rho loop of giant_advance).
+// 1/b with one Newton step from the MUFU.RCP64H seed.  Measured on B200
+// (bench_tools/rcp64_accuracy.cu, 1.6e8 samples): seed 2^-19.9, one step
+// 2^-39.9, two steps exact.  One step suffices wherever the quotient stays
+// below 2^38.8 (rint of an exact quotient: error < 0.5) or a floor is
+// corrected by one exact remainder test (quotient below 2^39.8): the rho loop,
+// w2, the divisions by By, x, G, H, u1 and the canonical shift below.  Their
+// bounds at d <= 1e11 (Q2 > 50): |w2| < d/100 < 2^30, |cx| < 2^21,
+// |dx| < 2^33, |dy| < 2^34, (b m + l By)/H < 2^38; every quotient is checked
+// by its remainder (dexact_div) anyway, so a violation fails the call.
+// Only cy = Q2/bx keeps the two-step reciprocal (no small bound on it).
 EIS_HD double rcp64_1(double b) {
 #ifdef __CUDA_ARCH__
     double r;
@@ -469,26 +476,26 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     float fbx0;
     EIS_PROF(4);
     if (F == 1.f) {                            // gcd(u1, u2) = 1: G = 1, Bx = m b
-        rBy = rcp64(By);
+        rBy = rcp64_1(By);
         fbx0 = (float)dfloor_mod(m * (double)fb, By, rBy);      // |m b| < 2^39
     } else {
         const float fs = fabsf((float)s);
         float fyy;
         const float Gf = fxgcd_x(fs, F, fyy);  // yy |s| = G (mod F)
         G = (double)Gf;
-        const double rG = rcp64(G);
+        const double rG = rcp64_1(G);
         By = rint(u1 * rG);
         Cy = rint(u2 * rG);
         Dy = rint(s * rG);
-        rBy = rcp64(By);
+        rBy = rcp64_1(By);
         EIS_PROF(5);
         if (Gf == F) {                         // F | s: G = F, Bx = m b
             fbx0 = (float)dfloor_mod(m * (double)fb, By, rBy);
         } else {                               // Alg. 2 l.630-634, all reduced mod H first
             EIS_PROF(1);
-            const double H = rint((double)F * rG), rH = rcp64(H);
+            const double H = rint((double)F * rG), rH = rcp64_1(H);
             const double b = fb;
-            const double c = dexact_div(fma(-b, u2, (double)F), u1, rcp64(u1), err);
+            const double c = dexact_div(fma(-b, u2, (double)F), u1, rcp64_1(u1), err);
             const double yy = s < 0.0 ? -(double)fyy : (double)fyy;
             const double inner = dfloor_mod(
                 fma(dfloor_mod(b, H, rH), dfloor_mod(w1, H, rH),
@@ -524,7 +531,7 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
         const double dx = dexact_div(fma(Dy, bx, -w2 * x), By, rBy, err);
         const double Q3 = y * dx;
         const double Q4 = Q3 + Dy;
-        const double dy = dexact_div(Q4, x, rcp64(x), err);
+        const double dy = dexact_div(Q4, x, rcp64_1(x), err);
         double cy;
         if (bx != 0.0) cy = dexact_div(Q2, bx, rcp64(bx), err);
         else cy = dexact_div(fma(cx, dy, -w1), dx, rcp64(dx), err);
@@ -554,9 +561,9 @@ EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, 
     const float Gf = fxgcd_x(fabsf((float)v), (float)u, fyy);   // fyy |v| = G (mod u)
     warp_reconverge(wmask);
     const double G = (double)Gf;
-    const double rG = rcp64(G);
+    const double rG = rcp64_1(G);
     const double By = rint(u * rG), Dy = rint(v * rG);
-    const double rBy = rcp64(By);
+    const double rBy = rcp64_1(By);
     const double yy = v < 0.0 ? -(double)fyy : (double)fyy;
     const double Bx = dfloor_mod(dfloor_mod(yy, By, rBy) * dfloor_mod(w, By, rBy), By, rBy);
     // partial Euclid (Alg. 3 l.694-700) in exact FP32, as in nucomp_d
@@ -585,7 +592,7 @@ EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, 
         const double dx = dexact_div(fma(bx, Dy, -w * x), By, rBy, err);
         const double Q1 = dx * y;
         const double dy0 = Q1 + Dy;
-        const double dy = dexact_div(dy0, x, rcp64(x), err);
+        const double dy = dexact_div(dy0, x, rcp64_1(x), err);
         o.v3 = G * (dy0 + Q1) - sq + by * by;
         o.u3 = fma(by, by, -G * y * dy);
         o.w3 = fma(bx, bx, -G * x * dx);          // w3 = bx^2 - ax dx
@@ -637,7 +644,7 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
         ok = nudupl_d((double)(Q1 >> 1), -(double)P1, (double)m1.w, (float)L, o, err, dmask);
     } else {
         const double dd = (double)d;
-        const double w2 = rint(((double)P2 * (double)P2 - dd) * rcp64(2.0 * (double)Q2));   // exact
+        const double w2 = rint(((double)P2 * (double)P2 - dd) * rcp64_1(2.0 * (double)Q2));   // exact
         ok = nucomp_d((double)(Q1 >> 1), -(double)P1, (double)m1.w, (double)(Q2 >> 1),
                       -(double)P2, w2, (float)L, o, err, fmask);
     }
@@ -653,7 +660,7 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     }
     const double Qd = fabs(2.0 * o.u3);
     const double sd = (double)s;
-    const double Ps = sd - dfloor_mod(sd + o.v3, Qd, rcp64(Qd));
+    const double Ps = sd - dfloor_mod(sd + o.v3, Qd, rcp64_1(Qd));
     r.Q = (i64)Qd;
     r.P = (i64)Ps;
     // t(gamma) = DLOG[(x + y (v3-1)/2) mod 2][y mod 2] (R12)
