@@ -82,6 +82,10 @@ EIS_HD double dfloor_mod(double a, double b, double rb) {   // b > 0, result in 
     return r;
 }
 
+// a symmetric residue of a mod b (fp64 integers, b > 0, |a / b| < 2^38, rb ~ 1/b
+// to 2^-39.9): a - rint(a rb) b, in [-b/2 - b 2^-2, b/2 + b 2^-2]; exact (fma)
+EIS_HD double smod(double a, double b, double rb) { return fma(-rint(a * rb), b, a); }
+
 // 32-bit floor division for 0 <= a < 2^23, 0 < b < 2^23 (same float trick as
 // the baby step: round(a/b) by one FFMA, then one correction).
 EIS_HD u32 udiv23(u32 a, u32 b) {
@@ -497,10 +501,12 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
             const double b = fb;
             const double c = dexact_div(fma(-b, u2, (double)F), u1, rcp64_1(u1), err);
             const double yy = s < 0.0 ? -(double)fyy : (double)fyy;
-            const double inner = dfloor_mod(
-                fma(dfloor_mod(b, H, rH), dfloor_mod(w1, H, rH),
-                    dfloor_mod(c, H, rH) * dfloor_mod(w2, H, rH)), H, rH);
-            const double l = dfloor_mod(dfloor_mod(yy, H, rH) * inner, H, rH);
+            // l = yy (b w1 + c w2) mod H in symmetric residues (|r| <= H/2, three
+            // instructions each; any representative of l makes b m + l By
+            // divisible by H, which dexact_div checks): |b|, |c|, |yy| < 2^19,
+            // H < 2^19, so every product below is exact (< 2^38)
+            const double inner = smod(fma(b, smod(w1, H, rH), c * smod(w2, H, rH)), H, rH);
+            const double l = smod(yy * inner, H, rH);
             const double Bx = dexact_div(fma(b, m, l * By), H, rH, err);
             fbx0 = (float)dfloor_mod(Bx, By, rBy);
         }
@@ -565,7 +571,7 @@ EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, 
     const double By = rint(u * rG), Dy = rint(v * rG);
     const double rBy = rcp64_1(By);
     const double yy = v < 0.0 ? -(double)fyy : (double)fyy;
-    const double Bx = dfloor_mod(dfloor_mod(yy, By, rBy) * dfloor_mod(w, By, rBy), By, rBy);
+    const double Bx = dfloor_mod(smod(yy, By, rBy) * smod(w, By, rBy), By, rBy);   // (< 2^38)
     // partial Euclid (Alg. 3 l.694-700) in exact FP32, as in nucomp_d
     float fbx = (float)Bx, fby = (float)By, fx = 1.f, fy = 0.f;
     int z = 0;
