@@ -147,8 +147,13 @@ EIS_HD float ffloor_div_pos(float a, float b) {
 // floor-quotient loop (R36).  x is correct modulo b/g, which is all
 // NUCOMP uses (Alg. 2 l.626-634: b enters only through b u2 = F (mod u1)).
 constexpr float RMAGIC = 12582912.0f;  // 1.5 * 2^23: round to nearest for |v| < 2^22
+#ifndef EUCLID_UNROLL
+#define EUCLID_UNROLL 2                 // Euclid loops unrolled twice: +0.5% (4: +0.3%)
+#endif
+constexpr int kEuclidUnroll = EUCLID_UNROLL;
 EIS_HD float fxgcd_x(float a, float b, float &x) {
     float x0 = 1.f, x1 = 0.f;
+#pragma unroll kEuclidUnroll
     while (b != 0.f) {
         EIS_PROF(0);
         const float q = fmaf(a, rcp_approx(b), RMAGIC) - RMAGIC;
@@ -514,6 +519,7 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     // partial Euclid (Alg. 2 l.637-643) in exact FP32
     float fbx = fbx0, fby = (float)By, fx = 1.f, fy = 0.f;
     int z = 0;
+#pragma unroll kEuclidUnroll
     while (fby > L && fbx != 0.f) {
         EIS_PROF(2);
         const float q = ffloor_div_pos(fby, fbx);
