@@ -104,7 +104,14 @@ EIS_HD u32 entry_Q(u32 e) { return 4u * (e & 0x3FFFFu) + 2u; }
 EIS_HD u32 entry_t(u32 e) { return e >> 18; }
 // key = Q >> 2 identifies Q (Q = 2 mod 4 on reduced ideals)
 EIS_HD u32 entry_key(u32 e) { return e & 0x3FFFFu; }
-EIS_HD u32 slot_entry(u32 key, u32 j) { return key | ((j + 1) << 18); }
+// table slot of list entry e = key | t << 18 at index j: key (18 bits) | (j + 1) << 18
+// (11 bits; 0 marks an empty slot) | (t mod 3) << 29, so a hit reads t(theta_j)
+// from the slot instead of a second, dependent list load
+EIS_HD u32 slot_entry(u32 e, u32 j) {
+    return (e & 0x3FFFFu) | ((j + 1) << 18) | (entry_t(e) % 3u) << 29;
+}
+EIS_HD u32 slot_j1(u32 slot) { return (slot >> 18) & 0x7FFu; }   // j + 1
+EIS_HD u32 slot_t3(u32 slot) { return slot >> 29; }
 EIS_HD u32 store_bucket(u32 key, u32 nb) {         // multiply-shift hash onto [0, nb)
 #ifdef __CUDA_ARCH__
     return __umulhi(key * 0x9E3779B1u, nb);
@@ -123,7 +130,7 @@ EIS_HD void store_build_seq(u32 *tab, u32 nb, const u32 *list, u32 n) {
             u32 i = 0;
             while (i < (u32)BKT && tab[b * BKT + i] != 0) i++;
             if (i < (u32)BKT) {
-                tab[b * BKT + i] = slot_entry(key, j);
+                tab[b * BKT + i] = slot_entry(e, j);
                 break;
             }
             b = next_bucket(b, nb);
@@ -213,11 +220,11 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
             const int i = __builtin_ctz_portable(mm);
             mm &= mm - 1;
             const u32 e = first_slots ? first_slots[i] : tab[(size_t)p.b * BKT + i];
-            const u32 jj = ((e >> 18) & 0x7FFu) - 1;
+            const u32 jj = slot_j1(e) - 1;
             const u32 Qprev = jj ? entry_Q(list[jj - 1]) : 0u;
             const int k = match_kind(d, Q, P, s, jj, Qprev);
             if (k != HIT_NONE) {
-                t3 = jj ? mod3(entry_t(list[jj])) : 0u;   // t(theta), from the list
+                t3 = slot_t3(e);                          // t(theta_j) (0 for j = 0)
                 j = jj;
                 return k;
             }
@@ -742,7 +749,7 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
                     const u32 j = jb + 8 * lane + 4 * k + w;
                     const u32 e = w == 0 ? cur[k].x : (w == 1 ? cur[k].y : (w == 2 ? cur[k].z : cur[k].w));
                     const u32 key = entry_key(e);
-                    sv[i] = slot_entry(key, j);
+                    sv[i] = slot_entry(e, j);
                     bb[i] = store_bucket(key, nb);
                     const u32 pos = smem_atom_inc(cnt_s + 4 * bb[i]);
                     if (pos < (u32)BKT) smem_st(tab_s + 4 * (bb[i] * BKT + pos), sv[i]);
