@@ -1135,10 +1135,20 @@ constexpr int BSGS_THREADS = 256;
 struct BsgsSizes {
     int nw, j1, nb, lcap;
 };
+#ifndef NW_SNAP
+#define NW_SNAP 160
+#endif
 inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
     BsgsSizes z;
     const double w = alpha * std::pow((double)d_max, 0.25);   // window in nats
     z.nw = std::min(2040, std::max(16, ((int)(w / 1.22) + 7) & ~7));
+    // the store build reads the list in groups of 256 entries, and a group costs
+    // about as much as the baby steps of its entries: a window just past a
+    // multiple of 256 pays a whole extra group (at 1.5e10, nw 504 -> 520 cost
+    // the window kernel 14%).  Windows up to NW_SNAP entries past a multiple of
+    // 256 are cut back to it (measured: +0.9% at 2e9, +2.4% at 3e10, +2.5% at
+    // 5e10, neutral elsewhere; results never depend on nw, R6/R29)
+    if (z.nw > 256 && z.nw % 256 <= NW_SNAP) z.nw -= z.nw % 256;
     const double lnd = std::log((double)d_max);
     const double M = 2.0 * lnd + 4.0;
     const double msteps = 1.25 * M / 1.22;                      // M nats with slack

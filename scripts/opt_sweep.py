@@ -16,5 +16,9 @@ for combo in itertools.product(*vals):
     st = eis.get_stats()
     print(json.dumps({**dict(zip(keys, combo)), "E": int(cE[0]), "ms": round(st["total_ms"], 2),
                       "rate_M": round(st["d_classified"] / st["total_ms"] / 1e3, 1),
-                      "win": round(st.get("window_ms", 0), 2), "giant": round(st.get("giant_ms", 0), 2)}),
+                      "win": round(st.get("window_ms", 0), 2), "giant": round(st.get("giant_ms", 0), 2),
+                      "giant_per_d": round(st["giant_steps"] / max(st["d_classified"], 1), 2),
+                      "baby_per_d": round(st["baby_steps"] / max(st["d_classified"], 1), 1),
+                      "nw": st.get("window_nw"), "nb": st.get("window_nb"),
+                      "fallbacks": st["fallbacks"]}),
           flush=True)
