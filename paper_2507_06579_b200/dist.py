@@ -25,7 +25,7 @@ from . import shard_bounds as _shard_bounds
 
 # The AUTO path's crossover, which the "auto" split's cost model uses (the
 # library's option "crossover"; the model itself is in eis_shard_bounds).
-AUTO_CROSSOVER = 1_450_000_000
+AUTO_CROSSOVER = 1_100_000_000
 
 
 def shard_bounds(lo: int, hi: int, world: int, rank: int, balance: str = "flat") -> tuple[int, int]:
@@ -37,7 +37,7 @@ def shard_bounds(lo: int, hi: int, world: int, rank: int, balance: str = "flat")
     per-d cost grows like d^(1/4), so the cumulative cost grows like x^(5/4):
     cut points x_g = X (g/G)^(4/5).  balance="auto": equal cost under the
     measured cost of the AUTO path (HALF ~ d^(1/2) below the crossover, BSGS
-    ~ d^0.228 above), integrated numerically over (lo, hi].  Interior
+    ~ d^0.238 above), integrated numerically over (lo, hi].  Interior
     boundaries are multiples of 8 (never = 5 mod 8), so no candidate is split.
     """
     return _shard_bounds(lo, hi, world, rank, balance)
