@@ -1,3 +1,5 @@
+"""Per-call host wall and device time of count_window for fixed ranges under two
+bsgs_gb settings (scratch reservation behaviour when ranges alternate)."""
 import time, os, sys
 sys.path.insert(0, os.getcwd())
 import paper_2507_06579_b200 as eis
