@@ -10,21 +10,21 @@
 //                       counts depend on it), so the loop has no per-lane exit
 //                       test besides the symmetry exit (l.553-556).  Entries are
 //                       kept in registers in blocks of 8 (indices known at
-//                       compile time) and written as two 16-byte stores per lane
+//                       compile time) and written as one 32-byte store per lane
 //                       into a dense per-d list.  The same warp then builds the
 //                       32 stores, one d at a time, as bucketed hash tables in
-//                       shared memory from the (L2-resident) lists and writes
-//                       them out with coalesced 16-byte stores.
+//                       shared memory from the lists (read back in groups of 256
+//                       entries) and writes each out with one TMA bulk copy.
 //   bsgs_prep_kernel    k = 2 for every windowed d in lockstep (mu'_2 = mu_1^2,
 //                       NUDUPL, Alg. 4 l.745; R35 may make it the stride).
 //   bsgs_giant_kernel   persistent lanes with per-lane refill (giant counts are
 //                       heavy-tailed) and a software-pipelined lookup.
 //
-// The store ("dictionary of ideals", l.549, l.607).  list[j] = Q_j | t_j << 20 for
-// the j-th baby entry (theta_{j+1} <-> (Q_j, P_j); t unreduced, < 2^12).  The
+// The store ("dictionary of ideals", l.549, l.607).  list[j] = (Q_j >> 2) | t_j << 18
+// for the j-th baby entry (theta_{j+1} <-> (Q_j, P_j); t unreduced, < 2^14).  The
 // table is nb buckets of BKT = 16 slots (64 bytes, two DRAM sectors); slot =
-// (Q >> 2) | (j + 1) << 18, 0 = empty (Q = 2 mod 4 on reduced ideals, so Q >> 2
-// identifies Q); t_j is read from the list on a match.  An entry goes to the first free
+// (Q >> 2) | (j + 1) << 18 | (t_j mod 3) << 29, 0 = empty (Q = 2 mod 4 on reduced
+// ideals, so Q >> 2 identifies Q).  An entry goes to the first free
 // slot of bucket h(Q), else of the following buckets; slots fill in order, so
 // a lookup stops at the first empty slot.  P is not stored: on the principal
 // cycle P_j^2 = d - Q_{j-1} Q_j with P_j > 0 (rho), so a reduced (Q*, P*)
