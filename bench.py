@@ -57,6 +57,106 @@ def _load_json(rel: str):
         return None
 
 
+def compute_roofline(stats: dict, kms: dict, nD_rank: int, sm_clk: float, nsm: int) -> dict:
+    """The bench line's `roofline` object from one step's library statistics
+    (`eis_get_stats`), the per-kernel live spans `kms` (ms per step: walk,
+    sieve, window, giant), the d this rank classified, the sampled SM clock and
+    the SM count -- and the committed measurements UNIT_COUNTS, PIPE_PEAKS and
+    MEASURED_PEAKS.json.  Pure (no device): tests/test_measurement.py recomputes
+    the committed bench line's numbers with it."""
+    hz = sm_clk * 1e6
+    issue_peak_tops = nsm * ISSUE_WARP_PER_CLK_SM * 32 * hz / 1e12
+    bsgs = stats["giant_steps"] > 0
+    uc = _load_json(UNIT_COUNTS) or {}
+    pk = _load_json(PIPE_PEAKS) or {}
+    kc = uc.get("kernels", {})
+    pipe_peak = {p: pk["ops"][op]["warp_inst_per_clk_per_sm"] for p, op in PIPE_OF_PEAK.items()
+                 if op in pk.get("ops", {})}
+    hbm_peak = measured_hbm_gbs()
+
+    def kernel_roof(names, ms):
+        """Per-pipe and issue utilisation of a kernel family over its live span:
+        ncu's per-d warp-instruction counts (UNIT_COUNTS, the bench's scale) x
+        the d this rank classified per step / the live span, against the
+        measured per-pipe peaks (PIPE_PEAKS) at the sampled SM clock."""
+        if not ms or not all(nm in kc for nm in names):
+            return None
+        sec = ms / 1e3
+        warp = sum(kc[nm]["warp_inst_per_d"] for nm in names) * nD_rank
+        out = {"ms": ms, "issue": warp / sec / (nsm * ISSUE_WARP_PER_CLK_SM * hz),
+               "threads_per_inst": sum(kc[nm]["thread_inst_per_d"] for nm in names) * nD_rank / warp,
+               "pipes": {}}
+        for p, peak in pipe_peak.items():
+            w = sum(kc[nm]["pipe_warp_inst_per_d"][p] for nm in names) * nD_rank
+            out["pipes"][p] = w / sec / (nsm * peak * hz)
+        dram = sum(kc[nm]["dram_bytes_per_d"] for nm in names) * nD_rank
+        out["hbm_measured_bytes"] = dram / sec / 1e9 / hbm_peak
+        top = max(out["pipes"].items(), key=lambda kv: kv[1]) if out["pipes"] else ("-", 0)
+        out["top_pipe"] = {"pipe": top[0], "frac": top[1]}
+        return out
+
+    per_kernel = {"sieve": {"ms": kms["sieve"]}}
+    roofline = {}
+    if bsgs:
+        per_kernel["window"] = kernel_roof(["bsgs_window_kernel", "bsgs_prep_kernel"], kms["window"])
+        per_kernel["giant"] = kernel_roof(["bsgs_giant_kernel"], kms["giant"])
+        # the dominant kernel (the window kernel: the largest share of the
+        # serialised launch list, profiles/r02_*) is bound by HBM first:
+        # ncu puts its DRAM traffic at ~0.8 of the measured copy bandwidth,
+        # above its issue (~0.7) and any pipe (ALU ~0.55).  achieved =
+        # ALGORITHMIC bytes (SURVEY 8(d): the per-d store) per launch over
+        # the launch's live duration: list 4 nw + table 64 nb + records 40
+        # bytes per windowed d (nw, nb from the library's plan).
+        nw, nb = stats["window_nw"], stats["window_nb"]
+        alg = (4 * nw + 64 * nb + 40) * stats["windowed"]
+        wl = max(1, int(stats["kernel_launches"]) // 4)     # sieve, window, prep, giant per segment
+        traffic = (kc["bsgs_window_kernel"]["dram_bytes_per_d"] * nD_rank / wl
+                   if "bsgs_window_kernel" in kc else None)
+        achieved = alg / (kms["window"] / 1e3) / 1e9
+        roofline = {
+            "bound": "hbm", "kernel": "bsgs_window_kernel (+ bsgs_prep_kernel in its span)",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "traffic": traffic,
+            "basis": f"algorithmic bytes per windowed d = 4 nw + 64 nb + 40 (list, table, "
+                     f"records; nw={nw}, nb={nb}) x {stats['windowed']} d per step over the "
+                     f"live window span (CUDA events on its stream, {wl} launches per step); "
+                     f"peak = measured copy bandwidth (MEASURED_PEAKS.json); traffic = ncu "
+                     f"dram read+write per launch ({UNIT_COUNTS}); the list read-back by the "
+                     f"store build is not algorithmic (it mostly misses L2)",
+        }
+        # SURVEY 8(d)'s issue roofline of the whole walk (three kernels on two
+        # streams): 34 per baby step + c_g per giant step over the walk's span
+        cg = None
+        if "bsgs_giant_kernel" in kc and uc.get("giant_steps"):
+            cg = ((kc["bsgs_giant_kernel"]["thread_inst_per_d"] +
+                   kc["bsgs_prep_kernel"]["thread_inst_per_d"]) * uc["d"] / uc["giant_steps"])
+        if cg:
+            ops = GENERIC_PER_BABY * stats["baby_steps"] + cg * stats["giant_steps"]
+            a_t = ops / (kms["walk"] / 1e3) / 1e12
+            roofline["walk_issue"] = {
+                "achieved": a_t, "peak": issue_peak_tops, "unit": "T thread-ops/s",
+                "frac": a_t / issue_peak_tops,
+                "basis": f"{GENERIC_PER_BABY} per baby step + c_g = {cg:.0f} per giant step "
+                         f"(measured: giant + prep thread-instructions per giant step, "
+                         f"{UNIT_COUNTS}) over the walk's live span; peak = {nsm} SM x "
+                         f"{ISSUE_WARP_PER_CLK_SM:.0f} warp-inst/clk x 32 at the sampled "
+                         f"{sm_clk:.0f} MHz (FFMA alone issues 3.93 of the 4 per clock, {PIPE_PEAKS})"}
+    else:
+        per_kernel["half"] = {"ms": kms["window"]}
+        ops = 14 * stats["baby_steps"]
+        a_t = ops / (kms["window"] / 1e3) / 1e12
+        meas = kc.get("walk_half_kernel", {}).get("thread_inst_per_baby_step")
+        roofline = {"bound": "issue", "kernel": "walk_half_kernel", "achieved": a_t,
+                    "peak": issue_peak_tops, "unit": "T thread-ops/s", "frac": a_t / issue_peak_tops,
+                    "traffic": None,
+                    "basis": f"14 thread-instructions per rho step (the step's SASS, DESIGN.md 4; "
+                             f"ncu measures {meas and round(meas, 1)} per step with loop and "
+                             f"refill overhead, {UNIT_COUNTS})"}
+    roofline["per_kernel"] = per_kernel
+    roofline["per_kernel"] = per_kernel
+    return roofline
+
+
 def _env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -350,96 +450,8 @@ def main():
     if rank == 0:
         value = nD_job / (tot_ms_max / args.steps / 1e3)
         sm_clk = clocks.get("sm_mhz") or SM_MAX_MHZ_FALLBACK
-        hz = sm_clk * 1e6
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-        issue_peak_tops = nsm * ISSUE_WARP_PER_CLK_SM * 32 * hz / 1e12
-        bsgs = stats["giant_steps"] > 0
-        uc = _load_json(UNIT_COUNTS) or {}
-        pk = _load_json(PIPE_PEAKS) or {}
-        kc = uc.get("kernels", {})
-        pipe_peak = {p: pk["ops"][op]["warp_inst_per_clk_per_sm"] for p, op in PIPE_OF_PEAK.items()
-                     if op in pk.get("ops", {})}
-        hbm_peak = measured_hbm_gbs()
-
-        def kernel_roof(names, ms):
-            """Per-pipe and issue utilisation of a kernel family over its live span:
-            ncu's per-d warp-instruction counts (UNIT_COUNTS, the bench's scale) x
-            the d this rank classified per step / the live span, against the
-            measured per-pipe peaks (PIPE_PEAKS) at the sampled SM clock."""
-            if not ms or not all(nm in kc for nm in names):
-                return None
-            sec = ms / 1e3
-            warp = sum(kc[nm]["warp_inst_per_d"] for nm in names) * nD_rank
-            out = {"ms": ms, "issue": warp / sec / (nsm * ISSUE_WARP_PER_CLK_SM * hz),
-                   "threads_per_inst": sum(kc[nm]["thread_inst_per_d"] for nm in names) * nD_rank / warp,
-                   "pipes": {}}
-            for p, peak in pipe_peak.items():
-                w = sum(kc[nm]["pipe_warp_inst_per_d"][p] for nm in names) * nD_rank
-                out["pipes"][p] = w / sec / (nsm * peak * hz)
-            dram = sum(kc[nm]["dram_bytes_per_d"] for nm in names) * nD_rank
-            out["hbm_measured_bytes"] = dram / sec / 1e9 / hbm_peak
-            top = max(out["pipes"].items(), key=lambda kv: kv[1]) if out["pipes"] else ("-", 0)
-            out["top_pipe"] = {"pipe": top[0], "frac": top[1]}
-            return out
-
-        per_kernel = {"sieve": {"ms": kms["sieve"]}}
-        roofline = {}
-        if bsgs:
-            per_kernel["window"] = kernel_roof(["bsgs_window_kernel", "bsgs_prep_kernel"], kms["window"])
-            per_kernel["giant"] = kernel_roof(["bsgs_giant_kernel"], kms["giant"])
-            # the dominant kernel (the window kernel: the largest share of the
-            # serialised launch list, profiles/r02_*) is bound by HBM first:
-            # ncu puts its DRAM traffic at ~0.8 of the measured copy bandwidth,
-            # above its issue (~0.7) and any pipe (ALU ~0.55).  achieved =
-            # ALGORITHMIC bytes (SURVEY 8(d): the per-d store) per launch over
-            # the launch's live duration: list 4 nw + table 64 nb + records 40
-            # bytes per windowed d (nw, nb from the library's plan).
-            nw, nb = stats["window_nw"], stats["window_nb"]
-            alg = (4 * nw + 64 * nb + 40) * stats["windowed"]
-            wl = max(1, int(stats["kernel_launches"]) // 4)     # sieve, window, prep, giant per segment
-            traffic = (kc["bsgs_window_kernel"]["dram_bytes_per_d"] * nD_rank / wl
-                       if "bsgs_window_kernel" in kc else None)
-            achieved = alg / (kms["window"] / 1e3) / 1e9
-            roofline = {
-                "bound": "hbm", "kernel": "bsgs_window_kernel (+ bsgs_prep_kernel in its span)",
-                "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": traffic,
-                "basis": f"algorithmic bytes per windowed d = 4 nw + 64 nb + 40 (list, table, "
-                         f"records; nw={nw}, nb={nb}) x {stats['windowed']} d per step over the "
-                         f"live window span (CUDA events on its stream, {wl} launches per step); "
-                         f"peak = measured copy bandwidth (MEASURED_PEAKS.json); traffic = ncu "
-                         f"dram read+write per launch ({UNIT_COUNTS}); the list read-back by the "
-                         f"store build is not algorithmic (it mostly misses L2)",
-            }
-            # SURVEY 8(d)'s issue roofline of the whole walk (three kernels on two
-            # streams): 34 per baby step + c_g per giant step over the walk's span
-            cg = None
-            if "bsgs_giant_kernel" in kc and uc.get("giant_steps"):
-                cg = ((kc["bsgs_giant_kernel"]["thread_inst_per_d"] +
-                       kc["bsgs_prep_kernel"]["thread_inst_per_d"]) * uc["d"] / uc["giant_steps"])
-            if cg:
-                ops = GENERIC_PER_BABY * stats["baby_steps"] + cg * stats["giant_steps"]
-                a_t = ops / (kms["walk"] / 1e3) / 1e12
-                roofline["walk_issue"] = {
-                    "achieved": a_t, "peak": issue_peak_tops, "unit": "T thread-ops/s",
-                    "frac": a_t / issue_peak_tops,
-                    "basis": f"{GENERIC_PER_BABY} per baby step + c_g = {cg:.0f} per giant step "
-                             f"(measured: giant + prep thread-instructions per giant step, "
-                             f"{UNIT_COUNTS}) over the walk's live span; peak = {nsm} SM x "
-                             f"{ISSUE_WARP_PER_CLK_SM:.0f} warp-inst/clk x 32 at the sampled "
-                             f"{sm_clk:.0f} MHz (FFMA alone issues 3.93 of the 4 per clock, {PIPE_PEAKS})"}
-        else:
-            per_kernel["half"] = {"ms": kms["window"]}
-            ops = 14 * stats["baby_steps"]
-            a_t = ops / (kms["window"] / 1e3) / 1e12
-            meas = kc.get("walk_half_kernel", {}).get("thread_inst_per_baby_step")
-            roofline = {"bound": "issue", "kernel": "walk_half_kernel", "achieved": a_t,
-                        "peak": issue_peak_tops, "unit": "T thread-ops/s", "frac": a_t / issue_peak_tops,
-                        "traffic": None,
-                        "basis": f"14 thread-instructions per rho step (the step's SASS, DESIGN.md 4; "
-                                 f"ncu measures {meas and round(meas, 1)} per step with loop and "
-                                 f"refill overhead, {UNIT_COUNTS})"}
-        roofline["per_kernel"] = per_kernel
+        roofline = compute_roofline(stats, kms, nD_rank, sm_clk, nsm)
         roofline["walk_ms_per_step"] = kms["walk"]
         roofline["walk_share_of_step"] = kms["walk"] / (tot_ms_max / args.steps)
         window_field = None
@@ -480,7 +492,10 @@ def main():
             "window_call": window_field,
             "clocks": clocks,
             "stats_per_rank_step": {k: stats[k] for k in ("d_classified", "baby_steps",
-                                                          "giant_steps", "sym_exits", "windowed")},
+                                                          "giant_steps", "sym_exits", "windowed",
+                                                          "window_nw", "window_nb",
+                                                          "kernel_launches")},
+            "sm_count": nsm,
             "rank_d": nD_rank,
         }
         if world == 1 and not args.no_cpu_baseline:

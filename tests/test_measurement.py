@@ -65,3 +65,33 @@ def test_committed_unit_counts_are_consistent():
     assert 20 < k["bsgs_window_kernel"]["thread_inst_per_baby_step"] < 120
     assert 300 < k["bsgs_giant_kernel"]["thread_inst_per_giant_step"] < 3000
     assert uc["d"] > 10**6 and uc["giant_steps"] > uc["d"]
+
+
+def test_bench_roofline_recomputes_from_committed_files():
+    """Every roofline number of the committed bench line follows from the
+    line's own step statistics and live spans plus the committed measurements
+    (profiles/r02_unit_counts.json, r02_pipe_peaks.json, MEASURED_PEAKS.json),
+    through bench.compute_roofline (Roofline)."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    line = json.load(open(os.path.join(ROOT, "profiles", "r02_bench_n1.json")))
+    st = line["stats_per_rank_step"]
+    if "window_nw" not in st:
+        pytest.skip("bench line predates the recorded plan fields")
+    r = line["roofline"]
+    pk = r["per_kernel"]
+    kms = {"walk": r["walk_ms_per_step"], "sieve": pk["sieve"]["ms"], "window": pk["window"]["ms"],
+           "giant": pk["giant"]["ms"]}
+    again = bench.compute_roofline(st, kms, line["rank_d"], line["clocks"]["sm_mhz"],
+                                   line.get("sm_count", 148))
+    for key in ("achieved", "peak", "frac", "traffic"):
+        assert again[key] == pytest.approx(r[key], rel=1e-9), key
+    assert again["walk_issue"]["frac"] == pytest.approx(r["walk_issue"]["frac"], rel=1e-9)
+    for kern in ("window", "giant"):
+        for p, v in r["per_kernel"][kern]["pipes"].items():
+            assert again["per_kernel"][kern]["pipes"][p] == pytest.approx(v, rel=1e-9), (kern, p)
+    # the bound is the dominant kernel's highest utilisation in the committed ncu summary
+    assert r["bound"] == "hbm" and 0.3 < r["frac"] < 1.2
