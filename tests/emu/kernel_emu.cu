@@ -8,7 +8,8 @@
 // prints per d: "d t baby giant reduce fallback err kinds(plain,comp,dupl)"
 // MODE dupl (ALPHA_X16 = ideals per d): squares the first ideals of the principal
 // cycle with NUDUPL twice, the generic int64 nudupl() and the fp64 nudupl_d(),
-// and prints per d: "d checked mismatches err" (outputs u3 v3 x y G compared).
+// and prints per d: "d checked mismatches err" (outputs u3 v3 x y G compared;
+// both stop the partial Euclid at the fast path's bound, R38).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -32,12 +33,15 @@ int main(int argc, char **argv) {
             int checked = 0, bad = 0;
             BabyState st;
             const i64 L = (i64)isqrt_u64_dev((u64)isqrt_u64_dev(dd));
+            // the fast path stops its partial Euclid at kEuclidBound L (DESIGN.md
+            // R38); the generic nudupl() is given that bound as an integer
+            const i64 Lg = (i64)((float)L * kEuclidBound);
             if (!baby_init(st, dd, &r1)) {
                 for (int k = 0; k < per_d; k++) {
                     if ((i64)st.Q > plain_th) {
                         const Mu1Form m = mu1_form((i64)st.Q, (i64)st.P, (i64)dd, &err);
                         i64 u3, v3, w3, G, x, y;
-                        nudupl((i64)(m.Q >> 1), -(i64)m.P, m.w, L, u3, v3, w3, G, x, y, &err);
+                        nudupl((i64)(m.Q >> 1), -(i64)m.P, m.w, Lg, u3, v3, w3, G, x, y, &err);
                         CompD o;
                         nudupl_d((double)(m.Q >> 1), -(double)m.P, (double)m.w, (float)L, o, &err,
                                  0xffffffffu);

@@ -103,7 +103,8 @@ def test_verbatim_guard_case_661(emu):
 def test_fp64_nudupl_matches_generic_nudupl(emu):
     """The prep kernel's fp64 NUDUPL (forms.cuh nudupl_d, Alg. 3) gives
     the same (u3, v3, x, y, G) as the generic int64 nudupl() on the first 64
-    ideals of the principal cycle of seeded d up to 1e11. Its cofactor yy comes
+    ideals of the principal cycle of seeded d up to 1e11, both stopping the partial
+    Euclid at the fast path's bound (R38). Its cofactor yy comes
     from the nearest-integer xgcd (R36) and is used only mod u/G."""
     ds = np.concatenate([workloads.sample_candidates(lo, hi, 300, seed=11)
                          for lo, hi in ((10**6, 10**7), (10**9, 2 * 10**9), (9 * 10**10, 10**11))])
