@@ -108,7 +108,7 @@ EIS_HD u32 entry_key(u32 e) { return e & 0x3FFFFu; }
 // (11 bits; 0 marks an empty slot) | (t mod 3) << 29, so a hit reads t(theta_j)
 // from the slot instead of a second, dependent list load
 EIS_HD u32 slot_entry(u32 e, u32 j) {
-    return (e & 0x3FFFFu) | ((j + 1) << 18) | (entry_t(e) % 3u) << 29;
+    return (e & 0x3FFFFu) | ((j + 1) << 18) | mod3_small(entry_t(e)) << 29;   // t < 2^14
 }
 EIS_HD u32 slot_j1(u32 slot) { return (slot >> 18) & 0x7FFu; }   // j + 1
 EIS_HD u32 slot_t3(u32 slot) { return slot >> 29; }
