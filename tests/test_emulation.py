@@ -115,3 +115,27 @@ def test_fp64_nudupl_matches_generic_nudupl(emu):
     assert rows[:, 1].sum() > 20000          # squarings compared
     assert rows[:, 2].sum() == 0             # mismatches
     assert rows[:, 3].sum() == 0             # invariant violations
+
+
+def test_giant_step_excess_inside_two_sided_margin(tmp_path):
+    """The two-sided window (R35) takes the giant stride 2 dist_1 with
+    margin M = 2 ln d + 4 nats, which needs 2M >= kappa_2 + kappa_k + log sqrt d +
+    (one rho step, < log sqrt d) for the giant-step excess kappa,
+    i.e. |kappa| <= 1.5 ln d + 4.  tests/emu/giant_kappa.cu measures kappa over 20
+    giant steps of seeded d with the kernels' composition (NUCOMP stopping at
+    1.6 L, R38) and reduction."""
+    exe = str(tmp_path / "giant_kappa")
+    subprocess.check_call(["nvcc", "-x", "cu", "-std=c++17", "-O2", "-gencode",
+                           "arch=compute_100a,code=sm_100a", "-o", exe,
+                           os.path.join(ROOT, "tests", "emu", "giant_kappa.cu")])
+    for lo, hi in ((1_200_000_000, 1_300_000_000), (9_900_000_000, 10**10),
+                   (99_900_000_000, 10**11)):
+        ds = workloads.sample_candidates(lo, hi, 400, seed=21)
+        out = subprocess.run([exe, "30", "20"], input="\n".join(str(int(d)) for d in ds),
+                             capture_output=True, text=True, check=True)
+        assert out.stderr == ""                                  # no invariant violations
+        f = out.stdout.split()
+        n, kmin, kmax = int(f[0]), float(f[4]), float(f[6])
+        assert n > 300
+        bound = 1.5 * np.log(hi) + 4.0
+        assert -bound < kmin <= 0.0 and kmax < 1.0, (lo, kmin, kmax, bound)
