@@ -1165,7 +1165,14 @@ inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
         if (j >= 7 && z.nw - j >= msteps && 2 * j - z.nw >= msteps) z.j1 = j;
     }
     z.nb = std::max(1, (int)std::ceil(z.nw / (BKT * BKT_LOAD)));
-    z.lcap = (z.nw + 31) & ~31;
+    // list row pitch: nw rounded up to 32 words, plus one 32-byte sector.  The
+    // pad measured +0.9% on the bench slab (nw = 488: pitch 1952 -> 1984 bytes;
+    // pads of 16 / 32 / 64 / 96 words +0.6..+0.8%, a 2048-byte pitch +0.1%),
+    // +0.4% at 2.5e9, neutral at 1e11 (Layout)
+#ifndef LCAP_PAD
+#define LCAP_PAD 8
+#endif
+    z.lcap = ((z.nw + 31) & ~31) + LCAP_PAD;
     return z;
 }
 
