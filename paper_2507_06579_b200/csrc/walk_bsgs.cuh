@@ -11,7 +11,7 @@
 //                       test besides the symmetry exit (l.553-556).  Entries are
 //                       kept in registers in blocks of 8 (indices known at
 //                       compile time) and written as one 32-byte store per lane
-//                       into a dense per-d list.  The same warp then builds the
+//                       into the d's list (rows or 64-entry tiles: ListRef).  The same warp then builds the
 //                       32 stores, one d at a time, as bucketed hash tables in
 //                       shared memory from the lists (read back in groups of 256
 //                       entries) and writes each out with one TMA bulk copy.
@@ -60,7 +60,9 @@ struct BsgsArgs {
     int nw;             // window entries per d (multiple of 8, <= 2040)
     int j1;             // entry index of mu_1 (= 7 mod 8: the end of a block)
     int nb;             // table buckets per d
-    int lcap;           // list stride per d (>= nw, multiple of 32)
+    int lcap;           // list words per d (>= nw, multiple of 8): a wave of 32 d owns 32 lcap
+    u32 lsh, lcs, lls;  // list layout (list_off): chunks of 2^lsh entries, chunk stride lcs,
+                        // lane stride lls (rows: lsh = 30, lls = lcap)
     int plain_th;       // Alg. 4 plain-product threshold on Q (paper: 50; kernels: PLAIN_TH)
     float giant_cap_mul;// giant-step cap = giant_cap_mul * (d^(1/4) + 10)
     int two_sided;      // R35: conjugate hits + doubled stride (0 = the paper's one-sided Alg. 1)
@@ -120,6 +122,36 @@ EIS_HD u32 store_bucket(u32 key, u32 nb) {         // multiply-shift hash onto [
 #endif
 }
 EIS_HD u32 next_bucket(u32 b, u32 nb) { return b + 1 == nb ? 0u : b + 1; }
+
+// List layout.  The 32 lists of a wave (32 consecutive survivors) share a
+// region of 32 lcap words.  Entry j of lane l's list sits at
+//   (j >> lsh) lcs + l lls + (j & (2^lsh - 1))
+// from the region's base: rows (lsh = 30, lls = lcap: each list contiguous) for
+// windows of one build group (nw <= 256), else tiles of 64 entries (lsh = 6,
+// lcs = 32 * 64, lls = 64: the warp's 32-byte block stores land in an 8 KB span
+// instead of 32 rows across 62 KB, and a list is read back in 256-byte pieces).
+// Measured against rows: +1.8% on the bench slab, +0.5% at 5e9, +2.1% at 3e10,
+// +2.4% at 1e11; tiles of 16 / 32 / 128 / 256 entries -8.6% / +0.7% / +1.6% /
+// -0.6% at 1e10, and with nw = 256 (1.5e9-2.5e9) tiles lose 2%, so rows stay
+// there.  The kernels are templates on the layout (LE = 0 rows, 64 tiles), so
+// the baby loop's block addresses are compile-time.  DESIGN.md 4, Layout.
+struct ListRef {
+    const u32 *base;    // the d's lane origin: wave region + l lls
+    u32 lsh, lcs;
+};
+EIS_HD u32 list_at(const ListRef &L, u32 j) {
+    return L.base[(j >> L.lsh) * L.lcs + (j & ((1u << L.lsh) - 1u))];
+}
+template <int LE>
+EIS_HD u32 list_off_t(u32 j) { return LE ? (j / LE) * (32u * LE) + j % LE : j; }
+// a flat list (host emulation): one row
+EIS_HD ListRef list_flat(const u32 *list) {
+    ListRef L;
+    L.base = list;
+    L.lsh = 30;
+    L.lcs = 0;
+    return L;
+}
 
 // host/emulation build: sequential insertion into a zeroed table
 EIS_HD void store_build_seq(u32 *tab, u32 nb, const u32 *list, u32 n) {
@@ -205,7 +237,7 @@ EIS_HD u32 filled_mask(const Probe &p) {
 // key match (about one per d) re-reads its slot and checks P (R34, R35).
 // first_slots (nullable): a copy of the first probed bucket (the giant kernel's
 // shared-memory buffer), read on a key match instead of global memory.
-EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d, u32 s,
+EIS_HD int store_resolve(const u32 *tab, const ListRef &list, u32 nb, Probe p, u64 d, u32 s,
                          u32 Q, u32 P, u32 &t3, u32 &j, const u32 *first_slots = nullptr) {
     const u32 qk = Q >> 2;
     for (;;) {
@@ -221,7 +253,7 @@ EIS_HD int store_resolve(const u32 *tab, const u32 *list, u32 nb, Probe p, u64 d
             mm &= mm - 1;
             const u32 e = first_slots ? first_slots[i] : tab[(size_t)p.b * BKT + i];
             const u32 jj = slot_j1(e) - 1;
-            const u32 Qprev = jj ? entry_Q(list[jj - 1]) : 0u;
+            const u32 Qprev = jj ? entry_Q(list_at(list, jj - 1)) : 0u;
             const int k = match_kind(d, Q, P, s, jj, Qprev);
             if (k != HIT_NONE) {
                 t3 = slot_t3(e);                          // t(theta_j) (0 for j = 0)
@@ -537,7 +569,7 @@ EIS_HD GiantInfo giant_start(GiantLane &g, const BsgsArgs &B, u32 *err, u32 wmas
 // true when the d is decided.
 EIS_HD bool giant_lookup(GiantLane &g, const u32 *tab, const u32 *list, const BsgsArgs &B) {
     u32 te, j;
-    const int kind = store_resolve(tab, list, B.nb, store_probe(tab, B.nb, g.Qc), g.d,
+    const int kind = store_resolve(tab, list_flat(list), B.nb, store_probe(tab, B.nb, g.Qc), g.d,
                                    (u32)g.s, g.Qc, g.Pc, te, j);
     if (kind != HIT_NONE) {
         g.phase = giant_hit(g, kind, te, g.tc, g.distc, g.Qc, g.res) ? PH_DONE : PH_HALF;
@@ -709,16 +741,18 @@ __device__ __forceinline__ void smem_st4_zero(u32 addr) {
 // One store, built by the whole warp in shared memory (tab: nb * BKT slots, cnt:
 // nb fill counters, both zero on entry and on exit) and written to dst.  A
 // group is 256 entries, 8 per lane (two uint4 per lane).
+template <int LE>
 __device__ __forceinline__ void load_group0(const u32 *lst, u32 n, uint4 (&nx)[2]) {
     const int lane = threadIdx.x & 31;
     nx[0] = nx[1] = make_uint4(0, 0, 0, 0);
-    if (lst && 8u * (u32)lane < n) list_ld8(lst + 8 * lane, nx[0], nx[1]);
+    if (lst && 8u * (u32)lane < n) list_ld8(lst + list_off_t<LE>(8 * lane), nx[0], nx[1]);
 }
 
 // nx: this d's first list group on entry (the caller or the previous call loaded
 // it); the next d's (lst_next) on exit, so list read-back latency overlaps the
 // previous d's inserts.
 // tab_s, cnt_s: shared-window addresses of the warp's table and counters.
+template <int LE>
 __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u32 *lst_next,
                                             u32 n, u32 nb, u32 tab_s, u32 cnt_s,
                                             u32 *__restrict__ dst, uint4 (&nx)[2]) {
@@ -731,9 +765,9 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
         if (jb + 128 * K < n) {
             const u32 j8 = jb + 128 * K + 8u * (u32)lane;
             nx[0] = nx[1] = make_uint4(0, 0, 0, 0);
-            if (j8 < n) list_ld8(lst + j8, nx[0], nx[1]);
+            if (j8 < n) list_ld8(lst + list_off_t<LE>(j8), nx[0], nx[1]);
         } else {
-            load_group0(lst_next, n, nx);            // the next d's first group
+            load_group0<LE>(lst_next, n, nx);        // the next d's first group
         }
         // first attempts for the group's entries, then one warp-uniform loop for
         // full buckets (rare)
@@ -794,8 +828,21 @@ __device__ __forceinline__ void build_store(const u32 *__restrict__ lst, const u
 #ifndef WINDOW_MINB
 #define WINDOW_MINB 4                         // with the L2 hints: 3 / 4 / 5 / 6 CTAs per SM 436 / 436 / 433 / 427 M d/s
 #endif
+// LE: the list layout as a compile-time constant (0 rows, 64 tiles; B.lsh says
+// which): the baby loop's block stores then cost no runtime address arithmetic
+template <int LE>
+__device__ __forceinline__ ListRef list_ref_t(const u32 *lists, u64 idx, const BsgsArgs &B) {
+    ListRef L;
+    L.base = LE ? lists + (idx >> 5) * 32u * (u64)B.lcap + (idx & 31u) * (u64)LE
+                : lists + idx * (u64)B.lcap;
+    L.lsh = LE ? 6 : 30;
+    L.lcs = LE ? 32 * LE : 0;
+    return L;
+}
+template <int LE>
 __global__ void __launch_bounds__(256, WINDOW_MINB)
 bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
+    static_assert(LE == 0 || LE == 64, "list tiles are 64 entries (lsh = 6)");
     extern __shared__ u32 smem[];                       // histogram, then per-warp tables
     u32 *hist = smem;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -827,7 +874,8 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
             const u32 off0 = __ldg(a.list + idx);
             win_begin(w, cand_d(a.i0 + (off0 & ~PRIME_BIT)), e[0], e[1]);
         }
-        u32 *lst = o.lists + (u64)idx * B.lcap;
+        const ListRef Lw = list_ref_t<LE>(o.lists, idx, B);
+        u32 *lst = const_cast<u32 *>(Lw.base);
         if (w.live) baby += 7;                           // theta_2 (closed form) + 6
 #pragma unroll
         for (int k = 2; k < 8; k++) {
@@ -847,7 +895,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 if (k == 3 || k == 7) win_flush(w);
             }
             if (w.live) {
-                store_block(lst + blk * 8, e);
+                store_block(lst + list_off_t<LE>(blk * 8), e);
                 if (blk * 8 + 7 == B.j1) win_mark_mu1(w);
             }
         }
@@ -864,13 +912,14 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         const u32 live = __ballot_sync(FULL_MASK, w.live);
         uint4 nx[2];
         if (live)
-            load_group0(o.lists + (u64)(wave * 32 + (u32)(__ffs(live) - 1)) * B.lcap, (u32)B.nw, nx);
+            load_group0<LE>(list_ref_t<LE>(o.lists, wave * 32 + (u32)(__ffs(live) - 1), B).base,
+                            (u32)B.nw, nx);
         for (u32 m = live; m; m &= m - 1) {
             const u32 i = wave * 32 + (u32)(__ffs(m) - 1);
             const u32 m2 = m & (m - 1);
-            const u32 *next = m2 ? o.lists + (u64)(wave * 32 + (u32)(__ffs(m2) - 1)) * B.lcap
+            const u32 *next = m2 ? list_ref_t<LE>(o.lists, wave * 32 + (u32)(__ffs(m2) - 1), B).base
                                  : nullptr;
-            build_store(o.lists + (u64)i * B.lcap, next, (u32)B.nw, nb, tab_s, cnt_s,
+            build_store<LE>(list_ref_t<LE>(o.lists, i, B).base, next, (u32)B.nw, nb, tab_s, cnt_s,
                         o.tables + (u64)i * ((u64)nb * BKT), nx);
         }
         u32 qb = 0;
@@ -889,6 +938,7 @@ bsgs_window_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #ifndef PREP_MINB
 #define PREP_MINB 4                           // measured: 2 / 3 / 4 CTAs per SM: 340 / 342 / 343 M d/s
 #endif
+template <int LE>
 __global__ void __launch_bounds__(256, PREP_MINB)
 bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     extern __shared__ u32 hist[];                       // hist_words(a)
@@ -922,7 +972,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         // the generic path) in lockstep, so the giant kernel composes distinct ideals
         if (two) {
             const u32 *tab = o.tables + (u64)gidx * ((u64)B.nb * BKT);
-            const u32 *lst = o.lists + (u64)gidx * B.lcap;
+            const ListRef lst = list_ref_t<LE>(o.lists, gidx, B);
             u32 te, j;
             const int kind = store_resolve(tab, lst, B.nb, store_probe(tab, B.nb, g.Qc), g.d,
                                            (u32)g.s, g.Qc, g.Pc, te, j);
@@ -976,6 +1026,7 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 #define PLAIN_TH 50
 #endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
+template <int LE>
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
 bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     extern __shared__ u32 hist[];                       // hist_words(a)
@@ -1043,7 +1094,7 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
         if (g.phase == PH_GIANT) {
             // (pointers recomputed from the 32-bit index: fewer live registers)
             const u32 *tab = o.tables + (u64)gidx * ((u64)B.nb * BKT);
-            const u32 *list = o.lists + (u64)gidx * B.lcap;
+            const ListRef list = list_ref_t<LE>(o.lists, gidx, B);
             // software pipeline: probe mu'_k (refills start with mu'_2, not yet
             // probed) while computing mu'_{k+1}; the bucket is copied to shared
             // memory asynchronously (cp.async), so no registers wait across the
@@ -1134,6 +1185,7 @@ constexpr int BSGS_THREADS = 256;
 // more ideals (l.560).
 struct BsgsSizes {
     int nw, j1, nb, lcap;
+    u32 lsh, lcs, lls;      // list layout (ListRef)
 };
 #ifndef NW_SNAP
 #define NW_SNAP 160
@@ -1172,7 +1224,17 @@ inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
 #ifndef LCAP_PAD
 #define LCAP_PAD 8
 #endif
-    z.lcap = ((z.nw + 31) & ~31) + LCAP_PAD;
+    if (z.nw > 256) {                            // tiles of 64 entries (ListRef)
+        z.lcap = (z.nw + 63) & ~63;
+        z.lsh = 6;
+        z.lcs = 32 * 64;
+        z.lls = 64;
+    } else {                                     // rows
+        z.lcap = ((z.nw + 31) & ~31) + LCAP_PAD;
+        z.lsh = 30;
+        z.lcs = 0;
+        z.lls = (u32)z.lcap;
+    }
     return z;
 }
 
@@ -1234,6 +1296,9 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     B.j1 = z.j1;
     B.nb = z.nb;
     B.lcap = z.lcap;
+    B.lsh = z.lsh;
+    B.lcs = z.lcs;
+    B.lls = z.lls;
     B.plain_th = PLAIN_TH;
     B.giant_cap_mul = (float)giant_cap;
     B.two_sided = two_sided;
@@ -1250,20 +1315,22 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     pl.hist_smem = (size_t)hist_w * sizeof(u32);
     pl.window_smem =
         pl.hist_smem + (size_t)(BSGS_THREADS / 32) * window_smem_words((u32)z.nb) * sizeof(u32);
-    if (cudaFuncSetAttribute(bsgs_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(bsgs_window_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pl.window_smem) != cudaSuccess ||
+        cudaFuncSetAttribute(bsgs_window_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pl.window_smem) != cudaSuccess)
         return -4;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_window_kernel, BSGS_THREADS,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_window_kernel<64>, BSGS_THREADS,
                                                       pl.window_smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
     pl.window_blocks = (unsigned)(num_sms * (window_ctas > 0 ? std::min(window_ctas, per_sm) : per_sm));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_prep_kernel, BSGS_THREADS,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_prep_kernel<64>, BSGS_THREADS,
                                                       pl.hist_smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
     pl.prep_blocks = (unsigned)(num_sms * per_sm);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_giant_kernel, GIANT_THREADS,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsgs_giant_kernel<64>, GIANT_THREADS,
                                                       pl.hist_smem) != cudaSuccess ||
         per_sm < 1)
         return -4;
@@ -1274,14 +1341,23 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
 // window + prep on the main stream
 inline int bsgs_launch_baby(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t s) {
     if (cudaMemsetAsync(pl.o.ctr, 0, 4 * sizeof(u32), s) != cudaSuccess) return -4;
-    bsgs_window_kernel<<<pl.window_blocks, BSGS_THREADS, pl.window_smem, s>>>(a, pl.B, pl.o);
+    if (pl.B.lsh == 6)
+        bsgs_window_kernel<64><<<pl.window_blocks, BSGS_THREADS, pl.window_smem, s>>>(a, pl.B, pl.o);
+    else
+        bsgs_window_kernel<0><<<pl.window_blocks, BSGS_THREADS, pl.window_smem, s>>>(a, pl.B, pl.o);
     if (cudaGetLastError() != cudaSuccess) return -4;
-    bsgs_prep_kernel<<<pl.prep_blocks, BSGS_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
+    if (pl.B.lsh == 6)
+        bsgs_prep_kernel<64><<<pl.prep_blocks, BSGS_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
+    else
+        bsgs_prep_kernel<0><<<pl.prep_blocks, BSGS_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
 inline int bsgs_launch_giant(const WalkArgs &a, const BsgsPlan &pl, cudaStream_t s) {
-    bsgs_giant_kernel<<<pl.giant_blocks, GIANT_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
+    if (pl.B.lsh == 6)
+        bsgs_giant_kernel<64><<<pl.giant_blocks, GIANT_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
+    else
+        bsgs_giant_kernel<0><<<pl.giant_blocks, GIANT_THREADS, pl.hist_smem, s>>>(a, pl.B, pl.o);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 #endif  // __CUDACC__ (launch)

@@ -64,7 +64,9 @@ def combine(csv_path: str, stats_path: str, out_path: str) -> None:
         name = name[5:] if name.startswith("void ") else name
         if prefix_id is not None and r[h.index("ID")] != prefix_id:
             second_call = True                 # past the first call's prefix kernel
-        if name.startswith("walk_half_kernel"):
+        if name.startswith("bsgs_"):                         # (templates on the list layout)
+            name = name.split("<")[0]
+        elif name.startswith("walk_half_kernel"):
             name = "walk_half_kernel"
         elif second_call:                      # kernels of the HALF call
             name += " (HALF call)"
