@@ -546,28 +546,25 @@ EIS_HD bool nucomp_d(double u1, double v1, double w1, double u2, double v2, doub
     const double bx = fbx, by = fby, x = fx, y = fy;
     if (z == 0) EIS_PROF(6);
     if (bx == 0.0) EIS_PROF(7);
-    if (z != 0) {
-        const double cx = dexact_div(fma(Cy, bx, -m * x), By, rBy, err);
-        const double Q1 = by * cx;
-        const double Q2 = Q1 + m;
-        const double dx = dexact_div(fma(Dy, bx, -w2 * x), By, rBy, err);
-        const double Q3 = y * dx;
-        const double Q4 = Q3 + Dy;
-        const double dy = dexact_div(Q4, x, rcp64_1(x), err);
-        double cy;
-        if (bx != 0.0) cy = dexact_div(Q2, bx, rcp64(bx), err);
-        else cy = dexact_div(fma(cx, dy, -w1), dx, rcp64(dx), err);
-        o.u3 = fma(by, cy, -G * y * dy);
-        o.w3 = fma(bx, cx, -G * x * dx);          // w3 = bx cx - ax dx, ax = G x
-        o.v3 = G * (Q3 + Q4) - Q1 - Q2;
-    } else {
-        const double Q1 = Cy * bx;
-        const double cx = dexact_div(Q1 - m, By, rBy, err);
-        const double dx = dexact_div(fma(bx, Dy, -w2), By, rBy, err);
-        o.u3 = by * Cy;
-        o.w3 = fma(bx, cx, -G * dx);              // w3 = bx cx - G dx
-        o.v3 = v2 - 2.0 * Q1;
-    }
+    // Alg. 2 l.644-660 as one path: with no Euclid step (z = 0: x = 1, y = 0,
+    // by = By) the general formulas give cy = Cy, u3 = By Cy, v3 = v2 - 2 Cy bx,
+    // the z = 0 branch's values (Dy G + m = v2), and for bx = 0 the paper's
+    // alternative cy = (cx dy - w1)/dx is taken by a select (m Dy + w1 By = Cy w2
+    // from v_i^2 - 4 u_i w_i = d makes it Cy too when z = 0).  The warp used to
+    // run both branches whenever one lane needed the rare one.
+    const double cx = dexact_div(fma(Cy, bx, -m * x), By, rBy, err);
+    const double Q1 = by * cx;
+    const double Q2 = Q1 + m;
+    const double dx = dexact_div(fma(Dy, bx, -w2 * x), By, rBy, err);
+    const double Q3 = y * dx;
+    const double Q4 = Q3 + Dy;
+    const double dy = dexact_div(Q4, x, rcp64_1(x), err);
+    const bool bz = bx == 0.0;
+    const double cn = bz ? fma(cx, dy, -w1) : Q2, cd = bz ? dx : bx;
+    const double cy = dexact_div(cn, cd, rcp64(cd), err);
+    o.u3 = fma(by, cy, -G * y * dy);
+    o.w3 = fma(bx, cx, -G * x * dx);              // w3 = bx cx - ax dx, ax = G x
+    o.v3 = G * (Q3 + Q4) - Q1 - Q2;
     o.x = x;
     o.y = y;
     o.G = G;
@@ -606,20 +603,15 @@ EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, 
     warp_reconverge(wmask);
     const double bx = fbx, by = fby, x = fx, y = fy;
     const double sq = (bx + by) * (bx + by) - bx * bx;   // exact: < 2^40
-    if (z == 0) {
-        const double dx = dexact_div(fma(bx, Dy, -w), By, rBy, err);
-        o.u3 = by * by;
-        o.v3 = v - sq + o.u3;
-        o.w3 = fma(bx, bx, -G * dx);              // w3 = bx^2 - G dx
-    } else {
-        const double dx = dexact_div(fma(bx, Dy, -w * x), By, rBy, err);
-        const double Q1 = dx * y;
-        const double dy0 = Q1 + Dy;
-        const double dy = dexact_div(dy0, x, rcp64_1(x), err);
-        o.v3 = G * (dy0 + Q1) - sq + by * by;
-        o.u3 = fma(by, by, -G * y * dy);
-        o.w3 = fma(bx, bx, -G * x * dx);          // w3 = bx^2 - ax dx
-    }
+    // one path (Alg. 3 l.701-711): with no Euclid step (x = 1, y = 0) it gives
+    // u3 = by^2, v3 = G Dy - sq + by^2 = v - sq + u3, w3 = bx^2 - G dx: the z = 0 values
+    const double dx = dexact_div(fma(bx, Dy, -w * x), By, rBy, err);
+    const double Q1 = dx * y;
+    const double dy0 = Q1 + Dy;
+    const double dy = dexact_div(dy0, x, rcp64_1(x), err);
+    o.v3 = G * (dy0 + Q1) - sq + by * by;
+    o.u3 = fma(by, by, -G * y * dy);
+    o.w3 = fma(bx, bx, -G * x * dx);              // w3 = bx^2 - ax dx
     o.x = x;
     o.y = y;
     o.G = G;
@@ -692,10 +684,12 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     // log2|gamma|, gamma = G (a + y sqrt d)/(2 u3), a = 2 x u3 + y v3
     const double a = fma(2.0 * o.x, o.u3, o.y * o.v3);
     const float mag = fabsf((float)a) + fabsf((float)o.y) * sqrtd_f;
-    if ((a >= 0.0) == (o.y >= 0.0) || a == 0.0 || o.y == 0.0)
-        r.lg = log2_approx((float)o.G * mag / (float)Qd);
-    else   // |N(gamma)| = (Q1/2)(Q2/2)/|u3|, use the conjugate (no cancellation)
-        r.lg = log2_approx(2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1) / ((float)o.G * mag));
+    // |N(gamma)| = (Q1/2)(Q2/2)/|u3|: where a and y sqrt d cancel, the conjugate
+    // (no cancellation) gives log|gamma| = log|N| - log|conj gamma| (one log either way)
+    const bool direct = (a >= 0.0) == (o.y >= 0.0) || a == 0.0 || o.y == 0.0;
+    const float gm = (float)o.G * mag;
+    r.lg = log2_approx(direct ? gm / (float)Qd
+                              : 2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1) / gm);
     r.kind = fdup ? 2u : 1u;
     if (((r.Q & 3) != 2) | ((r.P & 1) != 1) | (((i64)o.G & 1) == 0) |
         !disc_ok(o.u3, o.v3, o.w3, (double)d))
