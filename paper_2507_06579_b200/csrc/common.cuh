@@ -157,6 +157,8 @@ struct WalkArgs {
     int n_ckpt;
     int nrow;            // count rows (2 or NROW_MAX)
     u32 hist_w;          // hist_words_of(ckpt, nrow, nb), set on the host
+    u64 ck_x0, ck_step;  // ck_step > 0: x[b_lo + i] = ck_x0 + i ck_step on this segment's
+    double ck_rstep;     // buckets (checkpoints in arithmetic progression), 1 / ck_step
     u64 *buckets;        // device: [nrow][n_ckpt] counts (row order above)
     u64 *stats;          // device: EisStatSlot counters
     u32 *err;            // device: invariant-violation counter
@@ -191,9 +193,21 @@ __device__ __forceinline__ void hist_zero(const WalkArgs &a, u32 *hist) {
     for (int i = threadIdx.x; i < a.nrow * a.nb; i += blockDim.x) hist[i] = 0;
 }
 // K4: one finished d into the CTA's shared-memory histogram
+// the bucket when the segment's checkpoints are an arithmetic progression: the
+// least i with d <= x0 + i step, from one fp64 quotient and exact integer
+// corrections (d - x0 < 2^53), instead of a binary search of dependent loads
+__device__ __forceinline__ int bucket_arith(const WalkArgs &a, u64 d) {
+    if (d <= a.ck_x0) return 0;
+    const u64 t = d - a.ck_x0;
+    u64 i = (u64)ceil((double)t * a.ck_rstep);
+    if (i * a.ck_step < t) i++;
+    else if (i > 0 && (i - 1) * a.ck_step >= t) i--;
+    return i < (u64)(a.nb - 1) ? (int)i : a.nb - 1;
+}
 __device__ __forceinline__ void hist_record(const WalkArgs &a, u32 *hist, u64 d, u32 t,
                                             bool prime) {
-    const int b = bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
+    const int b = a.ck_step ? bucket_arith(a, d)
+                            : bucket_of(a.ckpt, a.b_lo, a.b_lo + a.nb - 1, d) - a.b_lo;
     atomicAdd(&hist[b], 1u);
     if (t == 0) atomicAdd(&hist[a.nb + b], 1u);
     if (a.nrow > 2) {

@@ -414,6 +414,20 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
         a.flags = fseg;
         a.ckpt = x_host ? x_dev : nullptr;
         a.b_lo = b_lo;
+        // checkpoints of this segment in arithmetic progression: bucket by division
+        a.ck_x0 = 0;
+        a.ck_step = 0;
+        a.ck_rstep = 0.0;
+        if (x_host && nb >= 1) {
+            const u64 x0 = x_host[b_lo], step = nb > 1 ? x_host[b_lo + 1] - x0 : 1;
+            bool ar = step > 0;
+            for (int i = 2; ar && i < (int)nb; i++) ar = x_host[b_lo + i] == x0 + (u64)i * step;
+            if (ar) {
+                a.ck_x0 = x0;
+                a.ck_step = step;
+                a.ck_rstep = 1.0 / (double)step;
+            }
+        }
         a.nb = nb;
         a.n_ckpt = n;
         a.nrow = nrow;
