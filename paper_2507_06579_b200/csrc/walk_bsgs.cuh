@@ -1025,6 +1025,9 @@ bsgs_prep_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
 // 4.1 M violations over C5; the paper's 50 is kept.)
 #define PLAIN_TH 50
 #endif
+#ifndef REC_Q
+#define REC_Q 1
+#endif
 constexpr u32 STASH = 32;                     // giant kernel: resume records per warp ring
 template <int LE>
 __global__ void __launch_bounds__(GIANT_THREADS, GIANT_MINB)
@@ -1035,7 +1038,20 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     __shared__ GiantRec stash[GIANT_THREADS / 32][STASH];
     __shared__ u32 sidx[GIANT_THREADS / 32][STASH];
     __shared__ uint4 pbuf[GIANT_THREADS][4];           // the bucket being probed, per lane
+    // per-warp statistics (shared memory: per-lane counters spilled) and the queue of
+    // finished d (REC_Q): recorded 32 at a time at full width, instead of in the
+    // divergent tail of the warp iteration where a finishing lane (about two per
+    // iteration) made the whole warp wait on its checkpoint search and atomics
+    __shared__ u32 wst[GIANT_THREADS / 32][4];         // giant, rho steps, done, fallbacks
+    __shared__ unsigned long long wbaby[GIANT_THREADS / 32];
+    __shared__ u32 rq_off[GIANT_THREADS / 32][64];
+    __shared__ u8 rq_res[GIANT_THREADS / 32][64];
     hist_zero(a, hist);
+    {
+        const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+        if (l < 4) wst[w][l] = 0;
+        if (l == 0) wbaby[w] = 0;
+    }
     __syncthreads();
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1047,9 +1063,8 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
     bool exhausted = false;
     u32 head = 0, tail = 0;                            // warp-uniform ring positions
     bool qdone = false;                                // the queue is drained
-    u64 baby = 0;                                      // (half-walk fallback steps)
-    u32 giant = 0, red = 0, done = 0, fb = 0;          // per-thread counts fit in 32 bits
     u32 err = 0;
+    u32 rq_n = 0;                                      // warp-uniform: finished d queued
 
     for (;;) {
         const u32 need = __ballot_sync(FULL_MASK, g.phase == PH_IDLE && !exhausted);
@@ -1112,8 +1127,13 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
             const GiantInfo gi = giant_advance(g, B, &err, gmask, false);
-            giant++;
-            red += gi.nred;
+            {
+                const u32 rs = __reduce_add_sync(gmask, gi.nred);
+                if (lane == __ffs(gmask) - 1) {
+                    wst[wid][0] += (u32)__popc(gmask);
+                    wst[wid][1] += rs;
+                }
+            }
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             Probe pr;
             pr.b = pb;
@@ -1131,21 +1151,53 @@ bsgs_giant_kernel(WalkArgs a, BsgsArgs B, BsgsOut o) {
                 g.phase = PH_HALF;
             }
             if (g.phase == PH_HALF) {     // exact half walk instead
-                fb++;
+                atomicAdd(&wst[wid][3], 1u);
                 const HalfOne h = half_walk_one(g.d);
             g.res = h.res;
-            baby += h.steps;
+            atomicAdd(&wbaby[wid], (unsigned long long)h.steps);
             err += h.err;
                 g.phase = PH_DONE;
             }
         }
-        if (g.phase == PH_DONE) {
+        if (REC_Q) {
+            const u32 dm = __ballot_sync(FULL_MASK, g.phase == PH_DONE);
+            if (dm) {
+                if (g.phase == PH_DONE) {
+                    const u32 p = rq_n + (u32)__popc(dm & lanemask_lt());
+                    rq_off[wid][p] = off;
+                    rq_res[wid][p] = (u8)(g.res % 3);
+                    g.phase = PH_IDLE;
+                }
+                rq_n += (u32)__popc(dm);
+                __syncwarp();
+                if (rq_n >= 32) {                         // record 32 in lockstep
+                    const u32 o2 = rq_off[wid][lane];
+                    record_result(a, hist, o2, cand_d(a.i0 + (o2 & ~PRIME_BIT)), rq_res[wid][lane]);
+                    __syncwarp();
+                    rq_n -= 32;
+                    if ((u32)lane < rq_n) {
+                        rq_off[wid][lane] = rq_off[wid][lane + 32];
+                        rq_res[wid][lane] = rq_res[wid][lane + 32];
+                    }
+                    if (lane == 0) wst[wid][2] += 32;
+                    __syncwarp();
+                }
+            }
+        } else if (g.phase == PH_DONE) {
             record_result(a, hist, off, g.d, g.res);
-            done++;
+            atomicAdd(&wst[wid][2], 1u);
             g.phase = PH_IDLE;
         }
     }
-    flush_stats(a, baby, giant, red, done, 0, fb, err);
+    if ((u32)lane < rq_n) {                             // the queue's remainder
+        const u32 o2 = rq_off[wid][lane];
+        record_result(a, hist, o2, cand_d(a.i0 + (o2 & ~PRIME_BIT)), rq_res[wid][lane]);
+    }
+    if (lane == 0) wst[wid][2] += rq_n;
+    __syncwarp();
+    const bool l0 = lane == 0;
+    flush_stats(a, l0 ? wbaby[wid] : 0, l0 ? wst[wid][0] : 0, l0 ? wst[wid][1] : 0,
+                l0 ? wst[wid][2] : 0, 0, l0 ? wst[wid][3] : 0, err);
     hist_flush(a, hist);
 }
 
