@@ -11,7 +11,8 @@
 //                       test besides the symmetry exit (l.553-556).  Entries are
 //                       kept in registers in blocks of 8 (indices known at
 //                       compile time) and written as one 32-byte store per lane
-//                       into the d's list (rows or 64-entry tiles: ListRef).  The same warp then builds the
+//                       into the d's list (rows or 64-entry tiles: ListRef).
+//                       The same warp then builds the
 //                       32 stores, one d at a time, as bucketed hash tables in
 //                       shared memory from the lists (read back in groups of 256
 //                       entries) and writes each out with one TMA bulk copy.
@@ -61,8 +62,7 @@ struct BsgsArgs {
     int j1;             // entry index of mu_1 (= 7 mod 8: the end of a block)
     int nb;             // table buckets per d
     int lcap;           // list words per d (>= nw, multiple of 8): a wave of 32 d owns 32 lcap
-    u32 lsh, lcs, lls;  // list layout (list_off): chunks of 2^lsh entries, chunk stride lcs,
-                        // lane stride lls (rows: lsh = 30, lls = lcap)
+    u32 lsh;            // list layout (ListRef): 6 = tiles of 64 entries, 30 = rows
     int plain_th;       // Alg. 4 plain-product threshold on Q (paper: 50; kernels: PLAIN_TH)
     float giant_cap_mul;// giant-step cap = giant_cap_mul * (d^(1/4) + 10)
     int two_sided;      // R35: conjugate hits + doubled stride (0 = the paper's one-sided Alg. 1)
@@ -126,10 +126,11 @@ EIS_HD u32 next_bucket(u32 b, u32 nb) { return b + 1 == nb ? 0u : b + 1; }
 // List layout.  The 32 lists of a wave (32 consecutive survivors) share a
 // region of 32 lcap words.  Entry j of lane l's list sits at
 //   (j >> lsh) lcs + l lls + (j & (2^lsh - 1))
-// from the region's base: rows (lsh = 30, lls = lcap: each list contiguous) for
-// windows of one build group (nw <= 256), else tiles of 64 entries (lsh = 6,
-// lcs = 32 * 64, lls = 64: the warp's 32-byte block stores land in an 8 KB span
-// instead of 32 rows across 62 KB, and a list is read back in 256-byte pieces).
+// from the region's base: rows (lsh = 30, lls = lcap, lcs unused: each list
+// contiguous) for windows of one build group (nw <= 256), else tiles of 64
+// entries (lsh = 6, lcs = 32 * 64, lls = 64: the warp's 32-byte block stores
+// land in an 8 KB span instead of 32 rows across 62 KB, and a list is read back
+// in 256-byte pieces).  ListRef holds a d's origin (region + l lls), lsh, lcs.
 // Measured against rows: +1.8% on the bench slab, +0.5% at 5e9, +2.1% at 3e10,
 // +2.4% at 1e11; tiles of 16 / 32 / 128 / 256 entries -8.6% / +0.7% / +1.6% /
 // -0.6% at 1e10, and with nw = 256 (1.5e9-2.5e9) tiles lose 2%, so rows stay
@@ -1237,7 +1238,7 @@ constexpr int BSGS_THREADS = 256;
 // more ideals (l.560).
 struct BsgsSizes {
     int nw, j1, nb, lcap;
-    u32 lsh, lcs, lls;      // list layout (ListRef)
+    u32 lsh;                // list layout (ListRef): 6 = tiles of 64 entries, 30 = rows
 };
 #ifndef NW_SNAP
 #define NW_SNAP 160
@@ -1283,13 +1284,9 @@ inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
     if (z.nw > 256) {                            // tiles of 64 entries (ListRef)
         z.lcap = (z.nw + 63) & ~63;
         z.lsh = 6;
-        z.lcs = 32 * 64;
-        z.lls = 64;
     } else {                                     // rows
         z.lcap = ((z.nw + 31) & ~31) + LCAP_PAD;
         z.lsh = 30;
-        z.lcs = 0;
-        z.lls = (u32)z.lcap;
     }
     return z;
 }
@@ -1353,8 +1350,6 @@ inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int al
     B.nb = z.nb;
     B.lcap = z.lcap;
     B.lsh = z.lsh;
-    B.lcs = z.lcs;
-    B.lls = z.lls;
     B.plain_th = PLAIN_TH;
     B.giant_cap_mul = (float)giant_cap;
     B.two_sided = two_sided;
