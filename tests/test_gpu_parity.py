@@ -60,6 +60,8 @@ def test_flags_prefix_1e6(mode):
     (10**7 - 123_457, 10**7 + 77_777),            # ragged ends around 1e7
     (10**8 - 65_001, 10**8 + 3),                  # ~8k candidates at 1e8
     (10**9 - 16_003, 10**9 + 9),                  # 1e9
+    (2_500_000_000 - 8_003, 2_500_000_000),       # AUTO's BSGS with list rows (nw = 256)
+    (5 * 10**9 - 8_003, 5 * 10**9 + 5),           # 64-entry list tiles, nw 448
     (10**10 - 6_001, 10**10),                     # 1e10
     (eis.MAX_D - 1_203, eis.MAX_D),               # the top: 10^11
 ])
