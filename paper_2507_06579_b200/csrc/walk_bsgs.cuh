@@ -1252,8 +1252,10 @@ inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
     // multiple of 256 pays a whole extra group (at 1.5e10, nw 504 -> 520 cost
     // the window kernel 14%).  Windows up to NW_SNAP entries past a multiple of
     // 256 are cut back to it (measured: +0.9% at 2e9, +2.4% at 3e10, +2.5% at
-    // 5e10, neutral elsewhere; results never depend on nw, R6/R29)
-    if (z.nw > 256 && z.nw % 256 <= NW_SNAP) z.nw -= z.nw % 256;
+    // 5e10, neutral elsewhere; results never depend on nw, R6/R29).  Between 256
+    // and 512 the cut is 128 (with tiled lists, 448 beats 256 at 2.5e9 by 1.5% and
+    // at 3e9 by 3.3%, while 1.5e9 still prefers 256).
+    if (z.nw > 256 && z.nw % 256 <= (z.nw < 512 ? 128 : NW_SNAP)) z.nw -= z.nw % 256;
     // past one group the lists are tiled in 64-entry chunks (ListRef), so a window
     // is rounded up to a whole chunk: +0.5% at 5e9, +0.7% on the bench slab (nw 488
     // -> 512), +0.1% at 1e11
