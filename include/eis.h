@@ -203,7 +203,7 @@ enum { EIS_BALANCE_FLAT = 0, EIS_BALANCE_PREFIX = 1, EIS_BALANCE_AUTO = 2 };
  *  FLAT   equal widths (windows, where the cost per d is flat);
  *  PREFIX equal cost under a d^(1/4) cost model: cut points lo + (hi-lo)(g/G)^(4/5);
  *  AUTO   equal cost under the measured cost model of EIS_MODE_AUTO (HALF ~ d^(1/2)
- *         below option "crossover", BSGS ~ d^0.238 above), integrated numerically.
+ *         below option "crossover", BSGS ~ d^0.224 above), integrated numerically.
  * Interior cut points are multiples of 8 (never a candidate), so no candidate
  * is split; the shards of ranks 0..world-1 are disjoint and cover (lo, hi].
  * Host-only (no device needed).  Bad world/rank/balance, lo > hi -> EIS_EINVAL. */

@@ -66,9 +66,9 @@ struct Ctx {
     int comm_world = 1, comm_rank = 0;
     // options
     int mode = EIS_MODE_AUTO;
-    u64 crossover = 1100000000ULL;   // AUTO: HALF below, BSGS at/above (measured on B200, round 2:
-                                     // HALF 1.02x faster at 1e9, BSGS 1.02x at 1.2e9, 1.07x at
-                                     // 1.45e9, 1.14x at 2e9, 1.8x at 1e10)
+    u64 crossover = 750000000ULL;    // AUTO: HALF below, BSGS at/above (measured on B200, end of
+                                     // round 2, 1e8-wide windows: HALF 1.01x faster at 7e8, BSGS
+                                     // 1.02x at 8e8, 1.07x at 1e9, 1.09x at 1.1e9)
     int alpha_x16 = 0;               // BSGS baby window W = alpha d^(1/4); 0 = by d (alpha_for)
     int segment_log2 = 25;
     int blocks_per_sm = 4;           // measured: 4 >= 6 >= 8 (K3 HALF)
@@ -613,12 +613,13 @@ int count_window_rows(u64 lo, const u64 *x, size_t n, int nrow, u64 *out) {
 
 // Relative device time per candidate at d of the AUTO path (measured on one
 // B200): HALF below the crossover, rate ~ 2.68e8 (1e10/d)^(1/2)
-// d/s; BSGS at and above it, rate ~ 4.84e8 (1e10/d)^0.238 d/s.  Only the
+// d/s; BSGS at and above it, rate ~ 5.0e8 (1e10/d)^0.224 d/s (fitted to 8e8-1e11
+// at the end of round 2, within 7%).  Only the
 // shape matters for splitting.
 double auto_cost_density(double d) {
     d = std::max(d, 1.0);
     return d < (double)g.crossover ? std::pow(d / 1e10, 0.5) / 2.68e8
-                                   : std::pow(d / 1e10, 0.238) / 4.84e8;
+                                   : std::pow(d / 1e10, 0.224) / 5.0e8;
 }
 
 // cut point g of (lo, hi] into `world` contiguous shards, a multiple of 8

@@ -25,7 +25,7 @@ from . import shard_bounds as _shard_bounds
 
 # The AUTO path's crossover, which the "auto" split's cost model uses (the
 # library's option "crossover"; the model itself is in eis_shard_bounds).
-AUTO_CROSSOVER = 1_100_000_000
+AUTO_CROSSOVER = 750_000_000
 
 
 def shard_bounds(lo: int, hi: int, world: int, rank: int, balance: str = "flat") -> tuple[int, int]:

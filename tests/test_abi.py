@@ -87,7 +87,7 @@ def test_validation_before_device_work(lib):
     for k in ("two_sided", "bsgs_gb", "window_ctas", "giant_ctas", "crossover", "giant_cap"):
         eis.set_option(k, eis.get_option(k))          # every documented option round-trips
     # the measured defaults DESIGN.md section 2 / 4 states
-    assert eis.get_option("crossover") == 1_100_000_000
+    assert eis.get_option("crossover") == 750_000_000
     assert eis.get_option("bsgs_gb") == 48
     assert eis.get_option("two_sided") == 1 and eis.get_option("mode") == eis.MODE_AUTO
     from paper_2507_06579_b200.dist import AUTO_CROSSOVER

@@ -106,15 +106,15 @@ def test_shard_bounds_properties():
 def auto_cost_density(d: np.ndarray) -> np.ndarray:
     """The AUTO path's measured per-d device cost, written out
     independently of the library's eis_shard_bounds: HALF below the crossover
-    at 2.68e8 (1e10/d)^(1/2) d/s, BSGS above it at 4.84e8 (1e10/d)^0.238 d/s."""
+    at 2.68e8 (1e10/d)^(1/2) d/s, BSGS above it at 5.0e8 (1e10/d)^0.224 d/s."""
     d = np.maximum(np.asarray(d, dtype=np.float64), 1.0)
-    return np.where(d < AUTO_CROSSOVER, (d / 1e10) ** 0.5 / 2.68e8, (d / 1e10) ** 0.238 / 4.84e8)
+    return np.where(d < AUTO_CROSSOVER, (d / 1e10) ** 0.5 / 2.68e8, (d / 1e10) ** 0.224 / 5.0e8)
 
 
 def test_auto_balance_equalises_model_cost():
     """balance="auto" (the distributed default): on the C5 prefix (0, 1e11] each
     of 8 shards carries 1/8 of the modelled AUTO-path device time (HALF below
-    the 1.1e9 crossover, BSGS above), to within the 8-aligned rounding."""
+    the 7.5e8 crossover, BSGS above), to within the 8-aligned rounding."""
     X, G = 10**11, 8
     cuts = [shard_bounds(0, X, G, r, "auto") for r in range(G)]
     xs = np.linspace(1.0, X, 200001)
