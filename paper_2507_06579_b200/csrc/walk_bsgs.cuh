@@ -360,7 +360,10 @@ EIS_HD u32 win_step(WinLane &w) {
         w.res = baby_result_f(w.st);
         w.live = false;
     }
-    return list_entry_key(f_to_key(w.st.Q), w.st.t2 >> 1);
+    // list_entry_key(key, t2 >> 1): t2 is even (it starts at 2 or 4 and grows by
+    // 2 or 4), so (t2 >> 1) << 18 = t2 << 17 and the key (< 2^18) and t fields do
+    // not overlap: one shift-add instead of shift, shift, or
+    return f_to_key(w.st.Q) + (w.st.t2 << 17);
 }
 
 // fold the pending multipliers into the distance (every 4 steps: entry j = 3 mod 4)
