@@ -25,9 +25,10 @@
 // for the j-th baby entry (theta_{j+1} <-> (Q_j, P_j); t unreduced, < 2^14).  The
 // table is nb buckets of BKT = 16 slots (64 bytes, two DRAM sectors); slot =
 // (Q >> 2) | (j + 1) << 18 | (t_j mod 3) << 29, 0 = empty (Q = 2 mod 4 on reduced
-// ideals, so Q >> 2 identifies Q).  An entry goes to the first free
-// slot of bucket h(Q), else of the following buckets; slots fill in order, so
-// a lookup stops at the first empty slot.  P is not stored: on the principal
+// ideals, so Q >> 2 identifies Q; bit 31 of a bucket's last slot is
+// SLOT_PASSED).  An entry goes to the first free slot of bucket h(Q), else of
+// the following buckets, and every bucket that turned it away is flagged; a
+// lookup scans its bucket and follows on only past a flagged one.  P is not stored: on the principal
 // cycle P_j^2 = d - Q_{j-1} Q_j with P_j > 0 (rho), so a reduced (Q*, P*)
 // matches entry j >= 1 iff Q* = Q_j and P*^2 = d - Q_{j-1} Q* (exact, u64);
 // entry 0 is (2, P_1), the only reduced ideal of norm 1 (R34).  The
