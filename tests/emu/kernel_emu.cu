@@ -108,6 +108,25 @@ int main(int argc, char **argv) {
                     res = w.res;
                 } else {
                     store_build_seq(tab.data(), (u32)B.nb, lst.data(), (u32)B.nw);
+                    // table invariant: every entry j is reached from its bucket h(key)
+                    // by following only buckets flagged SLOT_PASSED (counted as errors)
+                    for (int j = 0; j < B.nw; j++) {
+                        const u32 key = entry_key(lst[j]);
+                        u32 b = store_bucket(key, (u32)B.nb), hops = 0;
+                        for (;;) {
+                            bool found = false;
+                            for (int i = 0; i < BKT; i++) {
+                                const u32 sl = tab[b * BKT + i];
+                                if (sl && (sl & 0x3FFFFu) == key && slot_j1(sl) == (u32)j + 1) found = true;
+                            }
+                            if (found) break;
+                            if (!(tab[b * BKT + BKT - 1] & SLOT_PASSED) || ++hops > (u32)B.nb) {
+                                err++;
+                                break;
+                            }
+                            b = next_bucket(b, (u32)B.nb);
+                        }
+                    }
                     const BabyRec br = win_pack(w, 0, (u32)B.nw);
                     GiantLane g;
                     giant_init(g, B, d, br, &err);

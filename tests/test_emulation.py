@@ -56,6 +56,19 @@ def test_every_d_upto_2e5(emu, mode):
     assert rows[:, 6].sum() == 0 and rows[:, 5].sum() == 0     # no invariant errors / fallbacks
 
 
+def test_bsgs_tiny_tables_overflow_chains(emu):
+    """Three buckets (48 slots) for windows of ~32 entries: most buckets fill,
+    entries are turned away into the following buckets (which the build flags,
+    SLOT_PASSED) and lookups follow the flags through chains that wrap around
+    the table.  Every d in (1e5, 2e5] must still match the oracle."""
+    ds, want = D_in(100_000, 200_000)
+    rows = run(emu, ds, "bsgs", ns_log2=3)
+    bad = np.flatnonzero(rows[:, 1] != want)
+    assert bad.size == 0, [(int(ds[i]), int(rows[i, 1]), int(want[i])) for i in bad[:10]]
+    assert rows[:, 6].sum() == 0 and rows[:, 5].sum() == 0     # no errors, no missed hits
+    # (a lookup that missed its entry would run the d to the cap and the half walk)
+
+
 @pytest.mark.parametrize("two_sided", [1, 0])
 @pytest.mark.parametrize("scale", [10**7, 10**8, 10**9, 10**10, 10**11])
 def test_bsgs_samples_at_scale(emu, scale, two_sided):
