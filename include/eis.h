@@ -108,7 +108,10 @@ EIS_API const char *eis_last_error(void);
  *  "half_ksteps"   HALF walk: rho steps per lane between refills (0 = auto, 18/36/72/144)
  *  "two_sided"     BSGS: 1 (default) = the store is also matched against conjugates and
  *                  the giant stride is mu_1^2 (R35); 0 = the paper's one-sided
- *                  Algorithm 1 */
+ *                  Algorithm 1
+ *  "load_x100"     BSGS store table load factor x 100, in [30, 90] (default 62, the
+ *                  measured optimum); results never depend on it (tests raise it to
+ *                  force overflow chains) */
 EIS_API int eis_set_option(const char *key, int64_t value);
 EIS_API int64_t eis_get_option(const char *key);
 

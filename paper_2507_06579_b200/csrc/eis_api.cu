@@ -81,6 +81,7 @@ struct Ctx {
                                      // a range within 2 bsgs_gb GiB runs as one segment)
     int half_ksteps = 0;             // 0: chosen per segment from d
     int two_sided = 1;               // BSGS: two-sided window (R35); 0 = paper's Alg. 1
+    int load_x100 = BKT_LOAD_X100;   // BSGS table load factor x 100 (tests stress chains with it)
     // instrumentation of the last call
     eis_stats last{};
     float walk_ms_acc = 0.f;
@@ -306,7 +307,7 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     u64 seg_cap = SEG;
     if (bsgs) {
         const u64 per = bsgs_bytes_per_survivor(cand_d(i_last), alpha_for(cand_d(i_last)) / 16.0f,
-                                                g.two_sided);
+                                                g.two_sided, g.load_x100 / 100.f);
         const u64 total = i_last - i_first + 1;
         const u64 cap_bytes = (u64)g.bsgs_gb << 30;
         seg_cap = total * per <= 2 * cap_bytes ? total
@@ -324,8 +325,8 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
     // streams and reallocated tens of GiB on most segments of a prefix run)
     if (bsgs) {
         const u64 d_a = cand_d(i_first), d_b = cand_d(i_last);
-        const BsgsSizes za = bsgs_sizes(d_a, alpha_for(d_a) / 16.0f, g.two_sided);
-        const BsgsSizes zb = bsgs_sizes(d_b, alpha_for(d_b) / 16.0f, g.two_sided);
+        const BsgsSizes za = bsgs_sizes(d_a, alpha_for(d_a) / 16.0f, g.two_sided, g.load_x100 / 100.f);
+        const BsgsSizes zb = bsgs_sizes(d_b, alpha_for(d_b) / 16.0f, g.two_sided, g.load_x100 / 100.f);
         const int lcap = std::max(za.lcap, zb.lcap), nbk = std::max(za.nb, zb.nb);
         // if the device cannot hold two buffers of bsgs_gb, halve the segment
         // (results do not depend on it) down to 2^16 candidates
@@ -438,12 +439,14 @@ int run_range(u64 i_first, u64 i_last, u8 *flags_dev, const u64 *x_host, const u
             BsgsPlan pl;
             // scratch is (re)allocated only when it must grow: drain both streams then
             // (otherwise the giant kernel of the previous segment keeps running on aux)
-            if (bsgs_needs_grow(bf.bsgs, len, d_last, alpha_for(d_last), g.two_sided)) {
+            if (bsgs_needs_grow(bf.bsgs, len, d_last, alpha_for(d_last), g.two_sided,
+                                g.load_x100 / 100.f)) {
                 CUDA_TRY(cudaStreamSynchronize(g.aux));
                 CUDA_TRY(cudaStreamSynchronize(s));
             }
             int rc = bsgs_prepare(pl, len, d_last, g.num_sms, alpha_for(d_last), g.giant_ctas, g.two_sided, bf.bsgs,
-                                  bf.ctr + 2, g.window_ctas, hist_words(a), g.giant_cap);
+                                  bf.ctr + 2, g.window_ctas, hist_words(a), g.giant_cap,
+                                  g.load_x100 / 100.f);
             if (rc) return rc == EIS_ENOMEM ? fail(EIS_ENOMEM, "BSGS scratch allocation failed")
                               : fail(EIS_EDEVICE, "BSGS setup failed: %s",
                                      cudaGetErrorString(cudaGetLastError()));
@@ -761,6 +764,7 @@ void eis_finalize(void) {
     fresh.giant_cap = g.giant_cap;
     fresh.half_ksteps = g.half_ksteps;
     fresh.two_sided = g.two_sided;
+    fresh.load_x100 = g.load_x100;
     g = fresh;
 }
 
@@ -804,6 +808,9 @@ int eis_set_option(const char *key, int64_t v) {
     } else if (k == "two_sided") {
         if (v != 0 && v != 1) return fail(EIS_EINVAL, "two_sided must be 0 or 1");
         g.two_sided = (int)v;
+    } else if (k == "load_x100") {
+        if (v < 30 || v > 90) return fail(EIS_EINVAL, "load_x100 must be in [30, 90]");
+        g.load_x100 = (int)v;
     } else {
         return fail(EIS_EINVAL, "unknown option '%s'", key);
     }
@@ -824,6 +831,7 @@ int64_t eis_get_option(const char *key) {
     if (k == "giant_cap") return g.giant_cap;
     if (k == "half_ksteps") return g.half_ksteps;
     if (k == "two_sided") return g.two_sided;
+    if (k == "load_x100") return g.load_x100;
     return fail(EIS_EINVAL, "unknown option '%s'", key);
 }
 

@@ -1267,7 +1267,8 @@ struct BsgsSizes {
 #ifndef NW_SNAP
 #define NW_SNAP 160
 #endif
-inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
+// load: the table load factor (option "load_x100"; BKT_LOAD by default)
+inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided, float load = BKT_LOAD) {
     BsgsSizes z;
     const double w = alpha * std::pow((double)d_max, 0.25);   // window in nats
     z.nw = std::min(2040, std::max(16, ((int)(w / 1.22) + 7) & ~7));
@@ -1299,7 +1300,7 @@ inline BsgsSizes bsgs_sizes(u64 d_max, float alpha, int two_sided) {
         const int j = ((z.nw - (int)std::ceil(msteps)) & ~7) - 1;
         if (j >= 7 && z.nw - j >= msteps && 2 * j - z.nw >= msteps) z.j1 = j;
     }
-    z.nb = std::max(1, (int)std::ceil(z.nw / (BKT * BKT_LOAD)));
+    z.nb = std::max(1, (int)std::ceil(z.nw / (BKT * load)));
     // list row pitch: nw rounded up to 32 words, plus one 32-byte sector.  The
     // pad measured +0.9% on the bench slab (nw = 488: pitch 1952 -> 1984 bytes;
     // pads of 16 / 32 / 64 / 96 words +0.6..+0.8%, a 2048-byte pitch +0.1%),
@@ -1338,8 +1339,8 @@ struct BsgsPlan {
 // true if bsgs_prepare would (re)allocate scratch (the caller must then drain
 // every stream that may still use it)
 inline bool bsgs_needs_grow(const BsgsScratch &scr, u64 seg_len, u64 d_hi, int alpha_x16,
-                            int two_sided) {
-    const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided);
+                            int two_sided, float load = BKT_LOAD) {
+    const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided, load);
     const size_t n = (size_t)seg_len;
     return !scr.lists || n * (size_t)z.lcap > scr.lists_n ||
            n * (size_t)z.nb * BKT > scr.tables_n || n > scr.brecs_n || n > scr.grecs_n ||
@@ -1358,8 +1359,9 @@ inline int bsgs_reserve(BsgsScratch &scr, size_t n, int lcap, int nb) {
     return 0;
 }
 
-inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
-    const BsgsSizes z = bsgs_sizes(d_max, alpha, two_sided);
+inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided,
+                                      float load = BKT_LOAD) {
+    const BsgsSizes z = bsgs_sizes(d_max, alpha, two_sided, load);
     return (size_t)4 * z.lcap + (size_t)64 * z.nb + sizeof(BabyRec) + sizeof(GiantRec) + 8;
 }
 
@@ -1368,9 +1370,9 @@ inline size_t bsgs_bytes_per_survivor(u64 d_max, float alpha, int two_sided) {
 // the launch shapes.  ctr: 4 device counters (zeroed by bsgs_launch_window).
 inline int bsgs_prepare(BsgsPlan &pl, u64 seg_len, u64 d_hi, int num_sms, int alpha_x16,
                         int giant_ctas, int two_sided, BsgsScratch &scr, u32 *ctr,
-                        int window_ctas, u32 hist_w, int giant_cap = 20) {
+                        int window_ctas, u32 hist_w, int giant_cap = 20, float load = BKT_LOAD) {
     BsgsArgs &B = pl.B;
-    const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided);
+    const BsgsSizes z = bsgs_sizes(d_hi, alpha_x16 / 16.0f, two_sided, load);
     B.nw = z.nw;
     B.j1 = z.j1;
     B.nb = z.nb;

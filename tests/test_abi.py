@@ -84,11 +84,15 @@ def test_validation_before_device_work(lib):
     with pytest.raises(eis.EisError):
         eis.set_option("alpha_x16", 3)
     eis.set_option("alpha_x16", 0)
-    for k in ("two_sided", "bsgs_gb", "window_ctas", "giant_ctas", "crossover", "giant_cap"):
+    for k in ("two_sided", "bsgs_gb", "window_ctas", "giant_ctas", "crossover", "giant_cap",
+              "load_x100"):
         eis.set_option(k, eis.get_option(k))          # every documented option round-trips
     # the measured defaults DESIGN.md section 2 / 4 states
     assert eis.get_option("crossover") == 750_000_000
     assert eis.get_option("bsgs_gb") == 48
+    assert eis.get_option("load_x100") == 62
+    with pytest.raises(eis.EisError):
+        eis.set_option("load_x100", 95)
     assert eis.get_option("two_sided") == 1 and eis.get_option("mode") == eis.MODE_AUTO
     from paper_2507_06579_b200.dist import AUTO_CROSSOVER
     assert AUTO_CROSSOVER == eis.get_option("crossover")   # the shard cost model's split

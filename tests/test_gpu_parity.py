@@ -122,10 +122,13 @@ def test_count_matches_oracle_and_flags(mode):
 
 @pytest.mark.parametrize("opts", [{"two_sided": 0}, {"bsgs_gb": 1}, {"alpha_x16": 8},
                                   {"alpha_x16": 64, "two_sided": 0}, {"giant_cap": 0},
-                                  {"giant_cap": 0, "two_sided": 0}])
+                                  {"giant_cap": 0, "two_sided": 0}, {"load_x100": 90},
+                                  {"load_x100": 90, "two_sided": 0}])
 def test_bsgs_options_do_not_change_results(opts):
     """BSGS with the paper's one-sided Alg. 1 (two_sided=0), tiny store memory
-    (many segments), and extreme windows: flags equal the oracle's (R6, R29, R35)."""
+    (many segments), extreme windows, and nearly full tables (load 0.9: many
+    buckets turn entries away, so lookups follow the passed flags through
+    chains): flags equal the oracle's (R6, R29, R35)."""
     old = {k: eis.get_option(k) for k in opts}
     try:
         eis.set_option("mode", eis.MODE_BSGS)
