@@ -687,9 +687,11 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     // |N(gamma)| = (Q1/2)(Q2/2)/|u3|: where a and y sqrt d cancel, the conjugate
     // (no cancellation) gives log|gamma| = log|N| - log|conj gamma| (one log either way)
     const bool direct = (a >= 0.0) == (o.y >= 0.0) || a == 0.0 || o.y == 0.0;
+    // (an approximate reciprocal: an IEEE float division is a subroutine with a
+    // slow path, and distances are float estimates anyway)
     const float gm = (float)o.G * mag;
-    r.lg = log2_approx(direct ? gm / (float)Qd
-                              : 2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1) / gm);
+    const float num = direct ? gm : 2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1);
+    r.lg = log2_approx(num * rcp_approx(direct ? (float)Qd : gm));
     r.kind = fdup ? 2u : 1u;
     if (((r.Q & 3) != 2) | ((r.P & 1) != 1) | (((i64)o.G & 1) == 0) |
         !disc_ok(o.u3, o.v3, o.w3, (double)d))

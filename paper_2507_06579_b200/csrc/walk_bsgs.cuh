@@ -465,14 +465,13 @@ EIS_HD RhoState rho_begin(const GiantLane &g, const GiantComp &c) {
     r.P = (double)c.P;
     r.nred = 0;
     r.mag = 1.0;
-    r.rQ = 0.0;
-    r.C = 0.0;
-    if (c.Q - c.P > (i64)g.s) {                  // not reduced: C = (d - P^2)/Q
-        // |P| < Q + s may reach 2^28, so d - P^2 in int64; the quotient is < 2^37
-        // and the division exact, so rint recovers it
-        r.rQ = rcp64_1(r.Q);
-        r.C = rint((double)((i64)g.d - c.P * c.P) * r.rQ);
-    }
+    // C = (d - P^2)/Q for every lane, reduced or not (it is only used when the
+    // output needs rho steps, 25% of lanes, but the warp ran the branch in
+    // nearly every iteration: unconditional measured +0.5%).  |P| < Q + s may
+    // reach 2^28, so d - P^2 in int64; the quotient is < 2^37 and the division
+    // exact, so rint recovers it
+    r.rQ = rcp64_1(r.Q);
+    r.C = rint((double)((i64)g.d - c.P * c.P) * r.rQ);
     return r;
 }
 
