@@ -63,6 +63,17 @@ EIS_HD u32 f2u_bits(float f) {
 #endif
 }
 
+// the low 32 bits of an integer-valued double v, |v| < 2^51, without a
+// conversion (the XU pipe is narrow): v + 1.5 * 2^52 holds v in its low mantissa
+// bits, two's complement for v < 0
+EIS_HD u32 dlo32(double v) {
+#ifdef __CUDA_ARCH__
+    return (u32)__double2loint(v + 6755399441055744.0);
+#else
+    return (u32)(long long)v;
+#endif
+}
+
 // fma rounded toward zero (FFMA.RZ).  The host emulation computes the exact
 // product-sum in double (a 20-bit x 24-bit product plus 2^23 is exact there)
 // and truncates, which equals RZ to float for results in [2^23, 2^24).

@@ -622,7 +622,7 @@ EIS_HD bool nudupl_d(double u, double v, double w, float L, CompD &o, u32 *err, 
 // I2 != mu_1) followed by the canonical representative (R17): returns
 // Q = |2 u3| and P* = s - ((s + v3) mod Q) in (s - Q, s] (P = -v3 mod Q, l.753).
 struct GiantComp {
-    i64 Q, P;
+    double Q, P;       // integers (|P| < 2^29): the rho state works in fp64
     u32 tg, kind;
     float lg;
 };
@@ -646,8 +646,8 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
         EIS_PROF(8);
         const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th);
         *err += c.nerr;
-        r.Q = c.Q;
-        r.P = s - floor_mod(s - c.P, c.Q);
+        r.Q = (double)c.Q;
+        r.P = (double)(s - floor_mod(s - c.P, c.Q));
         r.tg = c.tg;
         r.lg = c.lg;
         r.kind = c.kind;
@@ -666,8 +666,8 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     if (!ok) {
         const Composed c = nucomp_choose(m1, Q2, P2, d, L, (double)sqrtd_f, plain_th);
         *err += c.nerr;
-        r.Q = c.Q;
-        r.P = s - floor_mod(s - c.P, c.Q);
+        r.Q = (double)c.Q;
+        r.P = (double)(s - floor_mod(s - c.P, c.Q));
         r.tg = c.tg;
         r.lg = c.lg;
         r.kind = c.kind;
@@ -676,11 +676,11 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     const double Qd = fabs(2.0 * o.u3);
     const double sd = (double)s;
     const double Ps = sd - dfloor_mod(sd + o.v3, Qd, rcp64_1(Qd));
-    r.Q = (i64)Qd;
-    r.P = (i64)Ps;
-    // t(gamma) = DLOG[(x + y (v3-1)/2) mod 2][y mod 2] (R12)
-    const i64 xi = (i64)o.x, yi = (i64)o.y, v3i = (i64)o.v3;
-    r.tg = t_gamma(xi, yi, v3i);
+    r.Q = Qd;
+    r.P = Ps;
+    // t(gamma) = DLOG[(x + y (v3-1)/2) mod 2][y mod 2] (R12), from the
+    // low bits of x, y, v3 (dlo32: no conversions)
+    r.tg = t_gamma(dlo32(o.x), dlo32(o.y), dlo32(o.v3));
     // log2|gamma|, gamma = G (a + y sqrt d)/(2 u3), a = 2 x u3 + y v3
     const double a = fma(2.0 * o.x, o.u3, o.y * o.v3);
     const float mag = fabsf((float)a) + fabsf((float)o.y) * sqrtd_f;
@@ -693,7 +693,7 @@ EIS_HD GiantComp giant_compose(const Mu1Form &m1, i64 Q2, i64 P2, i64 d, i64 s, 
     const float num = direct ? gm : 2.f * (float)(Q1 >> 1) * (float)(Q2 >> 1);
     r.lg = log2_approx(num * rcp_approx(direct ? (float)Qd : gm));
     r.kind = fdup ? 2u : 1u;
-    if (((r.Q & 3) != 2) | ((r.P & 1) != 1) | (((i64)o.G & 1) == 0) |
+    if (((dlo32(Qd) & 3) != 2) | ((dlo32(Ps) & 1) != 1) | ((dlo32(o.G) & 1) == 0) |
         !disc_ok(o.u3, o.v3, o.w3, (double)d))
         *err += 1;
     return r;

@@ -461,8 +461,8 @@ EIS_HD RhoState rho_begin(const GiantLane &g, const GiantComp &c) {
     RhoState r;
     r.t = mod3_small(g.t1 + g.tc + 3u - c.tg);   // theta(mu_k) = theta(mu_1) theta(mu'_{k-1}) / gamma
     r.dist = g.dist1 + g.distc - c.lg;
-    r.Q = (double)c.Q;
-    r.P = (double)c.P;
+    r.Q = c.Q;
+    r.P = c.P;
     r.nred = 0;
     r.mag = 1.0;
     // C = (d - P^2)/Q for every lane, reduced or not (it is only used when the
@@ -471,7 +471,8 @@ EIS_HD RhoState rho_begin(const GiantLane &g, const GiantComp &c) {
     // reach 2^28, so d - P^2 in int64; the quotient is < 2^37 and the division
     // exact, so rint recovers it
     r.rQ = rcp64_1(r.Q);
-    r.C = rint((double)((i64)g.d - c.P * c.P) * r.rQ);
+    const i64 Pi = (i64)c.P;
+    r.C = rint((double)((i64)g.d - Pi * Pi) * r.rQ);
     return r;
 }
 
@@ -511,8 +512,8 @@ EIS_HD void rho_end(GiantLane &g, RhoState &r, u32 *err) {
         if (fma(r.Q, r.C, r.P * r.P) != (double)g.d) *err += 1;   // exact (< 2^40)
     }
     g.k++;
-    g.Qc = (u32)r.Q;
-    g.Pc = (u32)r.P;
+    g.Qc = dlo32(r.Q);                           // (reduced: 0 < P < Q < 2^21)
+    g.Pc = dlo32(r.P);
     g.tc = r.t;
     g.distc = r.dist;
 }
